@@ -1,0 +1,130 @@
+/*
+ * igs_b200.h -- C ABI of the B200 (sm_100a) densification hot path of ImprovedGS+.
+ *
+ * One shared library, libigs_b200.so, built from paper_2603_08661_b200/csrc/*.cu.
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * (passed as void*), returns an igs_status (0 == IGS_OK) and never allocates:
+ * the caller owns every buffer, including the workspace, whose size the
+ * matching *_workspace_bytes() query reports.  All launches are asynchronous
+ * on `stream`; the functions that must report device-detected conditions
+ * write them to caller-provided DEVICE counters (no hidden host syncs).
+ *
+ * The reference (`splitkit`, /root/reference/pkg/src/splitkit) is pure
+ * Python; there is no reference C ABI.  Each entry point names the reference
+ * function it replaces (file:line); the Python drop-in in
+ * paper_2603_08661_b200/ keeps the reference names, arguments and exceptions
+ * and binds these symbols through ctypes.
+ */
+#ifndef IGS_B200_H
+#define IGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+enum igs_status {
+  IGS_OK = 0,
+  IGS_ERR_ARGUMENT = 1,     /* bad shape / size / pointer / flag combination   */
+  IGS_ERR_CUDA = 2,         /* a CUDA runtime call failed (see igs_last_cuda_error) */
+  IGS_ERR_WORKSPACE = 3,    /* workspace smaller than *_workspace_bytes()      */
+  IGS_ERR_UNSUPPORTED = 4   /* valid request this build does not implement      */
+};
+
+enum igs_dtype { IGS_F32 = 0, IGS_F64 = 1 };
+
+/* igs_edge_importance flags (io_cli.py:315-323 --no-nms / --no-median) */
+enum igs_edge_flags { IGS_EDGE_NO_NMS = 1, IGS_EDGE_NO_MEDIAN = 2 };
+
+/* selection policy (schedule.py:94, densify_controller.py:72-77) */
+enum igs_policy { IGS_POLICY_PRODUCT = 0, IGS_POLICY_EDGE = 1, IGS_POLICY_GRAD = 2 };
+
+/* LAS pre-pass flags (core.py:43-46, core.py:27-28) */
+enum igs_las_flags {
+  IGS_LAS_BAD_QUAT = 1,     /* zero or non-finite quaternion norm -> ValueError */
+  IGS_LAS_BAD_OPACITY = 2,  /* sigmoid(o)*beta outside (0,1)    -> ValueError   */
+  IGS_LAS_RENORM = 4        /* some |norm-1| > 1e-4: renormalise the whole batch */
+};
+
+const char* igs_strerror(int status);
+const char* igs_last_cuda_error(void);
+int igs_abi_version(void);
+
+/* ---- edge-importance map (edge_pipeline.py) ----------------------------- */
+
+/* Workspace for igs_edge_importance / igs_median_normalize over `batch` views of height x width. */
+int igs_edge_workspace_bytes(int64_t batch, int64_t height, int64_t width, int flags,
+                             size_t* bytes);
+
+/* importance_pipeline (edge_pipeline.py:128-135), batched over views with per-view medians.
+ * image: (batch, height, width, channels) contiguous, channels 3 (RGB -> Rec.601 gray,
+ * :42-49) or 1 (already gray, not clipped, :134), dtype IGS_F32/IGS_F64.
+ * blur_w25: the 5x5 weights of blur_kernel_5x5(sigma) (:52-59), host memory, row-major.
+ * out: (batch, height, width) float64.  height, width >= 3.  One fused persistent launch:
+ * gray -> blur -> Sobel -> NMS (-> median histogram -> radix select -> normalise). */
+int igs_edge_importance(const void* image, int in_dtype, int channels,
+                        int64_t batch, int64_t height, int64_t width,
+                        const double* blur_w25, int flags, double* out,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* Stage entry points, one kernel each (edge_pipeline.py:42-125); batched over views. */
+int igs_to_grayscale(const void* image, int in_dtype, int64_t batch, int64_t height,
+                     int64_t width, double* gray, void* stream);                 /* :42-49  */
+int igs_gaussian_blur_5x5(const double* gray, int64_t batch, int64_t height, int64_t width,
+                          const double* blur_w25, double* out, void* stream);    /* :62-67  */
+int igs_sobel_gradients(const double* gray, int64_t batch, int64_t height, int64_t width,
+                        double* magnitude, double* orientation, void* stream);   /* :70-83  */
+int igs_nms_thin(const double* magnitude, const double* orientation, int64_t batch,
+                 int64_t height, int64_t width, double* out, void* stream);      /* :86-114 */
+/* median_normalize (:117-125) of `batch` independent arrays of n values (in may == out).
+ * medians (device, nullable): receives each array's positive median (1.0 if none). */
+int igs_median_normalize(const double* in, int64_t batch, int64_t n, double* out,
+                         double* medians, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
+/* ---- budgeted candidate selection (densify_controller.py:66-106) -------- */
+
+int igs_select_workspace_bytes(int64_t n, size_t* bytes);
+
+/* grad_norm = grad_sum / accum_count (0 if accum_count == 0, :40-43).  Eligible: all
+ * (warmup != 0) or grad_norm > grad_threshold.  take = min(#eligible, take_cap) where the
+ * host computes take_cap = min(headroom, max(ceil(growth_cap*count - 1e-9), 0)) (:99-100).
+ * mask[i] = 1 for the `take` eligible entries ranked first by (score desc, index asc),
+ * i.e. np.argsort(-score, kind="stable") (:104).  counts (device int64[2]) receives
+ * {#eligible, take}. */
+int igs_select_candidates(const double* grad_sum, int64_t accum_count, const double* edge_score,
+                          int64_t n, double grad_threshold, int warmup, int policy,
+                          int64_t take_cap, uint8_t* mask, int64_t* counts,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- Long-Axis-Split (las_split.py:146-179) ----------------------------- */
+
+int igs_las_workspace_bytes(int64_t count, size_t* bytes);
+
+/* Pre-pass over the mask (1 byte per Gaussian): per-block split counts and their exclusive
+ * scan (slot ranks), plus the flags of enum igs_las_flags over the MASKED parents.
+ * summary (device int64[2]) receives {n_split, flags}.  Nothing in the scene is written. */
+int igs_las_prepare(const uint8_t* mask, const float* rotations, const float* opacity_logits,
+                    int64_t count, float beta, void* workspace, size_t workspace_bytes,
+                    int64_t* summary, void* stream);
+
+/* Split pass (run after igs_las_prepare on the same workspace and a host check of the
+ * summary): parent i <- +offset child (positions, log_scales, opacity_logits written in
+ * place); slot count + rank(i) <- -offset child with the parent's rotation and SH cloned.
+ * Columns are SoA float32 with capacity rows: positions (cap,3), log_scales (cap,3),
+ * rotations (cap,4), opacity_logits (cap,), sh (cap, sh_floats).  renormalize != 0 applies
+ * the batch-global quaternion renormalisation of core.py:45-46. */
+int igs_las_apply(float* positions, float* log_scales, float* rotations, float* opacity_logits,
+                  float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
+                  const uint8_t* mask, float alpha, float log_alpha, float log_gamma,
+                  float beta, int renormalize, void* workspace, size_t workspace_bytes,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IGS_B200_H */

@@ -1,0 +1,20 @@
+"""B200-native (sm_100a) densification hot path of ImprovedGS+ (arXiv 2603.08661).
+
+A drop-in for the densification path of the reference ``splitkit`` package
+(``/root/reference/pkg/src/splitkit``): the edge-importance map, budgeted
+split-candidate selection and Long-Axis-Split, with the reference's names,
+arguments and exceptions.  Host code is Python; the arithmetic runs in
+hand-written CUDA kernels in ``libigs_b200.so`` (C ABI: ``include/igs_b200.h``),
+bound with ctypes.  There is no CPU fallback.
+"""
+
+from .core import Scene3
+from .densify_controller import (EVENT_CSV_HEADER, DensifyEvent, DensifyStats,
+                                 accumulate_grads, densify_step, select_candidates)
+from .edge_pipeline import (GradientField, blur_kernel_5x5, gaussian_blur_5x5,
+                            importance_batch, importance_pipeline, median_normalize,
+                            nms_thin, sobel_gradients, to_grayscale)
+from .las_split import BudgetError, SplitConstants, las_split_batch, principal_axis
+from .schedule import DensifyConfig, is_densify_step, is_warmup_step
+
+__version__ = "0.1.0"

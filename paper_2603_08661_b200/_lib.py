@@ -1,0 +1,115 @@
+"""ctypes binding of libigs_b200.so (include/igs_b200.h) plus workspace/stream plumbing.
+
+The product path has no CPU fallback: if the shared library or a CUDA device
+is missing, every entry point raises ``RuntimeError`` naming what is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libigs_b200.so")
+
+IGS_OK, IGS_ERR_ARGUMENT, IGS_ERR_CUDA, IGS_ERR_WORKSPACE, IGS_ERR_UNSUPPORTED = range(5)
+IGS_F32, IGS_F64 = 0, 1
+IGS_EDGE_NO_NMS, IGS_EDGE_NO_MEDIAN = 1, 2
+IGS_POLICY = {"product": 0, "edge": 1, "grad": 2}
+IGS_LAS_BAD_QUAT, IGS_LAS_BAD_OPACITY, IGS_LAS_RENORM = 1, 2, 4
+
+_vp, _i64, _sz, _int, _dbl, _flt = C.c_void_p, C.c_int64, C.c_size_t, C.c_int, C.c_double, C.c_float
+_szp = C.POINTER(C.c_size_t)
+
+# name -> (restype, argtypes); the exported C ABI, one line per include/igs_b200.h symbol
+SIGNATURES = {
+    "igs_strerror": (C.c_char_p, [_int]),
+    "igs_last_cuda_error": (C.c_char_p, []),
+    "igs_abi_version": (_int, []),
+    "igs_edge_workspace_bytes": (_int, [_i64, _i64, _i64, _int, _szp]),
+    "igs_edge_importance": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _int, _vp, _vp, _sz,
+                                   _vp]),
+    "igs_to_grayscale": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp]),
+    "igs_gaussian_blur_5x5": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "igs_sobel_gradients": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "igs_nms_thin": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "igs_median_normalize": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "igs_select_workspace_bytes": (_int, [_i64, _szp]),
+    "igs_select_candidates": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _i64, _vp, _vp, _vp,
+                                     _sz, _vp]),
+    "igs_las_workspace_bytes": (_int, [_i64, _szp]),
+    "igs_las_prepare": (_int, [_vp, _vp, _vp, _i64, _flt, _vp, _sz, _vp, _vp]),
+    "igs_las_apply": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt, _flt,
+                             _flt, _int, _vp, _sz, _vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and type the C ABI.  Works without a GPU (symbol checks only)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise RuntimeError(
+                    f"{path} is missing: build it with `python -m paper_2603_08661_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(path)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype, fn.argtypes = res, args
+            _lib = lib
+    return _lib
+
+
+def lib():
+    """The library, after checking that a CUDA device is present."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2603_08661_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return load()
+
+
+def check(status: int, what: str):
+    if status == IGS_OK:
+        return
+    L = load()
+    msg = L.igs_strerror(status).decode()
+    if status == IGS_ERR_CUDA:
+        msg += f" ({L.igs_last_cuda_error().decode()})"
+    if status == IGS_ERR_ARGUMENT:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg}")
+
+
+def stream_handle(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+_ws: dict = {}
+
+
+def workspace(nbytes: int, device, tag: str) -> torch.Tensor:
+    """Caller-owned scratch (the library never allocates), cached per (device, stream, tag)."""
+    device = torch.device(device)
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream, tag)
+    buf = _ws.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _ws[key] = buf
+    return buf
+
+
+def query_size(fn, *args) -> int:
+    out = C.c_size_t(0)
+    check(fn(*args, C.byref(out)), fn.__name__)
+    return int(out.value)

@@ -1,0 +1,46 @@
+// C-ABI housekeeping: status strings, CUDA error capture, device queries.
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include "igs_common.cuh"
+
+namespace igs {
+
+static thread_local char g_cuda_error[256] = "";
+
+void set_cuda_error(cudaError_t e) {
+  snprintf(g_cuda_error, sizeof(g_cuda_error), "%s: %s", cudaGetErrorName(e),
+           cudaGetErrorString(e));
+}
+
+int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      cached = n;
+  }
+  return cached;
+}
+
+}  // namespace igs
+
+extern "C" {
+
+const char* igs_strerror(int status) {
+  switch (status) {
+    case IGS_OK: return "ok";
+    case IGS_ERR_ARGUMENT: return "invalid argument";
+    case IGS_ERR_CUDA: return "CUDA error";
+    case IGS_ERR_WORKSPACE: return "workspace too small";
+    case IGS_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+const char* igs_last_cuda_error(void) { return igs::g_cuda_error; }
+
+int igs_abi_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+// Long-Axis-Split on sm_100a.
+//
+// Replaces splitkit.las_split.las_split_batch and the helpers it calls
+// (/root/reference/pkg/src/splitkit/las_split.py:52-179, core.py:17-58,151-157).
+//
+//   las_prepare_kernel  one pass over the 1-byte mask: per-tile split counts
+//                       plus the batch flags of the masked parents (bad
+//                       quaternion, logit domain, the batch-global
+//                       renormalisation trigger of core.py:45-46).
+//   las_scan_kernel     exclusive scan of the tile counts -> slot offsets.
+//   las_apply_kernel    per tile: ballot-ranked masked parents; per parent the
+//                       float32 LAS arithmetic in numpy's operation order, the
+//                       in-place +offset child (positions, log_scales,
+//                       opacity_logits) and the appended -offset child at slot
+//                       count + rank; rotations are cloned with one 16-byte
+//                       access and the SH rows with warp-cooperative 16-byte
+//                       copies of the tile's compacted parent list.
+// The host reads {n_split, flags} between prepare and apply (one sync), raising
+// BudgetError / ValueError before any column is written, as the reference does.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "igs_common.cuh"
+
+namespace igs {
+namespace las {
+
+constexpr int NT = 256;
+constexpr int PER = 4;
+constexpr int TILE = NT * PER;  // Gaussians per block
+
+struct Layout {
+  size_t tile_cnt, tile_off, total;
+};
+
+Layout layout(long long count) {
+  Layout L;
+  long long tiles = (count + TILE - 1) / TILE;
+  L.tile_cnt = 0;
+  L.tile_off = align_up(sizeof(unsigned) * (size_t)(tiles + 1), 256);
+  L.total = L.tile_off + align_up(sizeof(unsigned long long) * (size_t)(tiles + 1), 256);
+  return L;
+}
+
+// numpy float32: norm = sqrt((q*q).sum(-1)), summed left to right.
+__device__ __forceinline__ float quat_norm(float4 q) {
+  float s = q.x * q.x;
+  s = s + q.y * q.y;
+  s = s + q.z * q.z;
+  s = s + q.w * q.w;
+  return sqrtf(s);
+}
+
+// sigmoid(o) * beta in float32 (core.py:17-21 then las_split.py:96).
+__device__ __forceinline__ float raw_opacity(float o, float beta) {
+  float e = expf(-o);
+  float s = 1.0f / (1.0f + e);
+  return s * beta;
+}
+
+__global__ void __launch_bounds__(NT) las_prepare_kernel(const uint8_t* __restrict__ mask,
+                                                         const float* __restrict__ rot,
+                                                         const float* __restrict__ opac,
+                                                         long long count, float beta,
+                                                         unsigned* tile_cnt,
+                                                         unsigned long long* summary) {
+  __shared__ unsigned warp_cnt[NT / 32];
+  const long long base = (long long)blockIdx.x * TILE;
+  unsigned local = 0, flags = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    long long i = base + j * NT + threadIdx.x;
+    if (i < count && mask[i]) {
+      ++local;
+      float4 q = reinterpret_cast<const float4*>(rot)[i];
+      float n = quat_norm(q);
+      if (!isfinite(n) || n == 0.0f) flags |= IGS_LAS_BAD_QUAT;
+      else if (fabsf(n - 1.0f) > 1e-4f) flags |= IGS_LAS_RENORM;
+      float r = raw_opacity(opac[i], beta);
+      if (!(r > 0.0f && r < 1.0f)) flags |= IGS_LAS_BAD_OPACITY;
+    }
+  }
+  unsigned w = __reduce_add_sync(0xffffffffu, local);
+  unsigned f = __reduce_or_sync(0xffffffffu, flags);
+  if (lane_id() == 0) {
+    warp_cnt[threadIdx.x >> 5] = w;
+    if (f) atomicOr(&summary[1], (unsigned long long)f);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int k = 0; k < NT / 32; ++k) t += warp_cnt[k];
+    tile_cnt[blockIdx.x] = t;
+  }
+}
+
+// Single block: exclusive scan of the tile counts; summary[0] = total.
+__global__ void __launch_bounds__(1024) las_scan_kernel(const unsigned* tile_cnt, long long tiles,
+                                                        unsigned long long* tile_off,
+                                                        unsigned long long* summary) {
+  __shared__ unsigned warp_sums[32];
+  unsigned long long carry = 0;
+  for (long long b = 0; b < tiles; b += blockDim.x) {
+    long long i = b + threadIdx.x;
+    unsigned v = i < tiles ? tile_cnt[i] : 0u;
+    unsigned tot;
+    unsigned ex = block_exclusive_scan(v, warp_sums, &tot);
+    if (i < tiles) tile_off[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) summary[0] = carry;
+}
+
+struct Consts {
+  float alpha, log_alpha, log_gamma, beta;
+};
+
+__global__ void __launch_bounds__(NT) las_apply_kernel(
+    float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ rot,
+    float* __restrict__ opac, float* __restrict__ sh, long long sh_floats, long long count,
+    const uint8_t* __restrict__ mask, Consts c, int renorm,
+    const unsigned long long* __restrict__ tile_off) {
+  __shared__ unsigned warp_cnt[PER * NT / 32];
+  __shared__ unsigned warp_pre[PER * NT / 32];
+  __shared__ long long src_idx[TILE];
+  __shared__ unsigned s_total;
+  const long long base = (long long)blockIdx.x * TILE;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  bool m[PER];
+  unsigned wrank[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    long long i = base + j * NT + threadIdx.x;
+    m[j] = i < count && mask[i];
+    unsigned bal = __ballot_sync(0xffffffffu, m[j]);
+    wrank[j] = __popc(bal & lanemask_lt());
+    if (lane == 0) warp_cnt[j * (NT / 32) + warp] = __popc(bal);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan over (sub-tile, warp) in index order
+    unsigned v = warp_cnt[threadIdx.x];
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (threadIdx.x >= (unsigned)o) x += y;
+    }
+    warp_pre[threadIdx.x] = x - v;
+    if (threadIdx.x == 31) s_total = x;
+  }
+  __syncthreads();
+  static_assert(PER * NT / 32 == 32, "one warp scans the tile");
+  const unsigned long long slot0 = (unsigned long long)count + tile_off[blockIdx.x];
+
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    if (!m[j]) continue;
+    const long long i = base + j * NT + threadIdx.x;
+    const unsigned r = warp_pre[j * (NT / 32) + warp] + wrank[j];
+    const long long dst = (long long)(slot0 + r);
+    src_idx[r] = i;
+
+    // _split_common (las_split.py:78-99)
+    float l0 = ls[3 * i], l1 = ls[3 * i + 1], l2 = ls[3 * i + 2];
+    int l = 0;  // np.argmax: first maximum (a NaN counts as the maximum)
+    float best = l0;
+    if (!(best != best)) {
+      if (l1 > best || l1 != l1) { l = 1; best = l1; }
+      if (!(best != best) && (l2 > best || l2 != l2)) { l = 2; best = l2; }
+    }
+    const float offset = expf(best) * c.alpha;
+    float cl0 = l0 + c.log_gamma, cl1 = l1 + c.log_gamma, cl2 = l2 + c.log_gamma;
+    const float cll = best + c.log_alpha;
+    if (l == 0) cl0 = cll; else if (l == 1) cl1 = cll; else cl2 = cll;
+    const float raw = raw_opacity(opac[i], c.beta);
+    const float co = logf(raw / (1.0f - raw));
+
+    // quat_to_rotmat (core.py:32-58), column l only (axis_displacement, las_split.py:62-75)
+    float4 q = reinterpret_cast<const float4*>(rot)[i];
+    float w = q.x, x = q.y, y = q.z, z = q.w;
+    if (renorm) {
+      float n = quat_norm(q);
+      w = w / n; x = x / n; y = y / n; z = z / n;
+    }
+    float c0, c1, c2;
+    if (l == 0) {
+      c0 = 1.0f - 2.0f * (y * y + z * z);
+      c1 = 2.0f * (x * y + w * z);
+      c2 = 2.0f * (x * z - w * y);
+    } else if (l == 1) {
+      c0 = 2.0f * (x * y - w * z);
+      c1 = 1.0f - 2.0f * (x * x + z * z);
+      c2 = 2.0f * (y * z + w * x);
+    } else {
+      c0 = 2.0f * (x * z + w * y);
+      c1 = 2.0f * (y * z - w * x);
+      c2 = 1.0f - 2.0f * (x * x + y * y);
+    }
+    const float d0 = c0 * offset, d1 = c1 * offset, d2 = c2 * offset;
+    const float p0 = pos[3 * i], p1 = pos[3 * i + 1], p2 = pos[3 * i + 2];
+
+    // parent slot <- +offset child
+    pos[3 * i] = p0 + d0;
+    pos[3 * i + 1] = p1 + d1;
+    pos[3 * i + 2] = p2 + d2;
+    ls[3 * i] = cl0;
+    ls[3 * i + 1] = cl1;
+    ls[3 * i + 2] = cl2;
+    opac[i] = co;
+    // appended slot <- -offset child
+    pos[3 * dst] = p0 - d0;
+    pos[3 * dst + 1] = p1 - d1;
+    pos[3 * dst + 2] = p2 - d2;
+    ls[3 * dst] = cl0;
+    ls[3 * dst + 1] = cl1;
+    ls[3 * dst + 2] = cl2;
+    opac[dst] = co;
+    reinterpret_cast<float4*>(rot)[dst] = q;
+  }
+  __syncthreads();
+
+  // SH clone of the tile's parents into consecutive appended rows.
+  const unsigned n = s_total;
+  if (n == 0 || sh_floats == 0) return;
+  if ((sh_floats & 3) == 0) {
+    const long long q4 = sh_floats >> 2;
+    const float4* src = reinterpret_cast<const float4*>(sh);
+    float4* dstp = reinterpret_cast<float4*>(sh);
+    const long long total = (long long)n * q4;
+    for (long long e = threadIdx.x; e < total; e += NT) {
+      long long k = e / q4, qq = e - k * q4;
+      float4 v = ld_stream_f4(src + src_idx[k] * q4 + qq);
+      __stcs(dstp + (long long)(slot0 + k) * q4 + qq, v);
+    }
+  } else {
+    const long long total = (long long)n * sh_floats;
+    for (long long e = threadIdx.x; e < total; e += NT) {
+      long long k = e / sh_floats, qq = e - k * sh_floats;
+      sh[(long long)(slot0 + k) * sh_floats + qq] = sh[src_idx[k] * sh_floats + qq];
+    }
+  }
+}
+
+}  // namespace las
+}  // namespace igs
+
+using namespace igs;
+
+extern "C" {
+
+int igs_las_workspace_bytes(int64_t count, size_t* bytes) {
+  if (!bytes || count < 0) return IGS_ERR_ARGUMENT;
+  *bytes = las::layout(count).total;
+  return IGS_OK;
+}
+
+int igs_las_prepare(const uint8_t* mask, const float* rotations, const float* opacity_logits,
+                    int64_t count, float beta, void* workspace, size_t workspace_bytes,
+                    int64_t* summary, void* stream) {
+  if (count < 0 || !summary) return IGS_ERR_ARGUMENT;
+  if (count > 0 && (!mask || !rotations || !opacity_logits)) return IGS_ERR_ARGUMENT;
+  if (count > 0 && ((uintptr_t)rotations & 15)) return IGS_ERR_ARGUMENT;
+  las::Layout L = las::layout(count);
+  if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  IGS_CUDA_TRY(cudaMemsetAsync(summary, 0, 2 * sizeof(int64_t), s));
+  if (count == 0) return IGS_OK;
+  long long tiles = (count + las::TILE - 1) / las::TILE;
+  unsigned* tile_cnt = (unsigned*)((char*)workspace + L.tile_cnt);
+  unsigned long long* tile_off = (unsigned long long*)((char*)workspace + L.tile_off);
+  las::las_prepare_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
+      mask, rotations, opacity_logits, count, beta, tile_cnt, (unsigned long long*)summary);
+  IGS_LAUNCH_CHECK();
+  las::las_scan_kernel<<<1, 1024, 0, s>>>(tile_cnt, tiles, tile_off,
+                                          (unsigned long long*)summary);
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
+int igs_las_apply(float* positions, float* log_scales, float* rotations, float* opacity_logits,
+                  float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
+                  const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,
+                  int renormalize, void* workspace, size_t workspace_bytes, void* stream) {
+  if (count < 0 || capacity < count || sh_floats < 0) return IGS_ERR_ARGUMENT;
+  if (count == 0) return IGS_OK;
+  if (!positions || !log_scales || !rotations || !opacity_logits || !mask) return IGS_ERR_ARGUMENT;
+  if (sh_floats > 0 && !sh) return IGS_ERR_ARGUMENT;
+  if (((uintptr_t)rotations & 15) || (sh_floats % 4 == 0 && ((uintptr_t)sh & 15)))
+    return IGS_ERR_ARGUMENT;
+  las::Layout L = las::layout(count);
+  if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
+  long long tiles = (count + las::TILE - 1) / las::TILE;
+  las::Consts c{alpha, log_alpha, log_gamma, beta};
+  las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
+      positions, log_scales, rotations, opacity_logits, sh, sh_floats, count, mask, c,
+      renormalize, (const unsigned long long*)((char*)workspace + L.tile_off));
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,155 @@
+"""Drop-in for ``splitkit.densify_controller`` on B200 (3D scenes).
+
+Same names and semantics as ``/root/reference/pkg/src/splitkit/
+densify_controller.py``; the statistics live on the device and selection is
+one cooperative radix-select launch (``igs_select_candidates``).
+``densify_step`` runs select -> LAS pre-pass -> ONE 32-byte device->host read
+({eligible, take, n_split, flags}) -> LAS apply, and returns the same
+``DensifyEvent`` as the reference.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import las_split as _las
+from .core import Scene3
+from .schedule import DensifyConfig, is_densify_step, is_warmup_step
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2603_08661_b200 needs a CUDA device; there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class DensifyStats:
+    """Per-primitive selection signals between densify events (densify_controller.py:23-51),
+    float64 on the device."""
+
+    def __init__(self, count: int, device=None):
+        self._device = torch.device(device) if device is not None else _dev()
+        self._grad_sum = torch.zeros(count, dtype=torch.float64, device=self._device)
+        self._accum_count = 0
+        self.edge_score = torch.zeros(count, dtype=torch.float64, device=self._device)
+
+    def __len__(self):
+        return self._grad_sum.shape[0]
+
+    @property
+    def grad_norm(self):
+        if self._accum_count == 0:
+            return torch.zeros_like(self._grad_sum)
+        return self._grad_sum / self._accum_count
+
+    def reset(self, count: int | None = None):
+        if count is None:
+            count = len(self)
+        self._grad_sum = torch.zeros(count, dtype=torch.float64, device=self._device)
+        self._accum_count = 0
+        self.edge_score = torch.zeros(count, dtype=torch.float64, device=self._device)
+
+    def set_edge_score(self, values):
+        v = torch.as_tensor(np.asarray(values) if not isinstance(values, torch.Tensor) else values)
+        self.edge_score.copy_(v.to(self._device, torch.float64).reshape(-1))
+
+
+def accumulate_grads(stats: DensifyStats, step_grad_norms) -> DensifyStats:
+    """Fold one iteration's gradient norms into the running mean (densify_controller.py:54-63)."""
+    x = step_grad_norms
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, dtype=np.float64))
+    t = t.to(stats._device, torch.float64)
+    if tuple(t.shape) != tuple(stats._grad_sum.shape):
+        raise ValueError(f"gradient norms length {tuple(t.shape)} does not match stats length "
+                         f"{tuple(stats._grad_sum.shape)}")
+    stats._grad_sum += t
+    stats._accum_count += 1
+    return stats
+
+
+def _take_cap(cfg: DensifyConfig, count: int, headroom: int) -> int:
+    """min(headroom, max(ceil(growth_cap*count - 1e-9), 0)) (densify_controller.py:99-100)."""
+    cap = math.ceil(cfg.growth_cap * count - 1e-9)
+    return min(headroom, max(cap, 0))
+
+
+def _launch_select(stats: DensifyStats, cfg: DensifyConfig, step: int, take_cap: int):
+    """Async select; returns (mask uint8 tensor, counts int64[2] device tensor)."""
+    n = len(stats)
+    L = _lib.lib()
+    mask = torch.empty(n, dtype=torch.uint8, device=stats._device)
+    counts = torch.zeros(2, dtype=torch.int64, device=stats._device)
+    nbytes = _lib.query_size(L.igs_select_workspace_bytes, n)
+    ws = _lib.workspace(nbytes, stats._device, "select")
+    _lib.check(L.igs_select_candidates(
+        stats._grad_sum.data_ptr(), stats._accum_count, stats.edge_score.data_ptr(), n,
+        float(cfg.grad_threshold), int(is_warmup_step(cfg, step)), _lib.IGS_POLICY[cfg.policy],
+        int(take_cap), mask.data_ptr(), counts.data_ptr(), ws.data_ptr(), ws.numel(),
+        _lib.stream_handle()), "select_candidates")
+    return mask, counts
+
+
+def select_candidates(stats: DensifyStats, cfg: DensifyConfig, step: int, headroom: int):
+    """Boolean mask (CUDA tensor) of the primitives to split (densify_controller.py:80-106)."""
+    if headroom < 0:
+        raise ValueError("headroom must be non-negative")
+    n = len(stats)
+    if headroom == 0 or n == 0:
+        return torch.zeros(n, dtype=torch.bool, device=stats._device)
+    take_cap = _take_cap(cfg, n, headroom)
+    if take_cap <= 0:
+        return torch.zeros(n, dtype=torch.bool, device=stats._device)
+    mask, _ = _launch_select(stats, cfg, step, take_cap)
+    return mask.view(torch.bool)
+
+
+def eligible_count(stats: DensifyStats, cfg: DensifyConfig, step: int) -> int:
+    """int(_eligible_mask(stats, cfg, step).sum()) (densify_controller.py:66-69)."""
+    if is_warmup_step(cfg, step):
+        return len(stats)
+    return int((stats.grad_norm > cfg.grad_threshold).sum())
+
+
+@dataclass(frozen=True)
+class DensifyEvent:
+    """Log record of one densify step (densify_controller.py:109-119)."""
+
+    step: int
+    eligible: int
+    split: int
+    count_after: int
+
+    def as_csv_row(self) -> str:
+        return f"{self.step},{self.eligible},{self.split},{self.count_after}"
+
+
+EVENT_CSV_HEADER = "step,eligible,split,count_after"
+
+
+def densify_step(scene, stats: DensifyStats, cfg: DensifyConfig, step: int) -> DensifyEvent:
+    """One densify event on a GPU 3D scene, in place (densify_controller.py:125-147)."""
+    if not is_densify_step(cfg, step):
+        raise ValueError(f"step {step} is not a densify step for this timetable")
+    if len(stats) != scene.count:
+        raise ValueError("stats length does not match scene count")
+    if not isinstance(scene, Scene3):
+        # Scene2 (2-D desk-scale harness) is out of scope for the B200 path
+        raise TypeError(f"unsupported scene type {type(scene).__name__}")
+    headroom = scene.capacity - scene.count
+    n = scene.count
+    take_cap = _take_cap(cfg, n, headroom) if (headroom > 0 and n > 0) else 0
+    c = cfg.split_constants
+    if take_cap > 0:
+        mask, counts = _launch_select(stats, cfg, step, take_cap)
+        prep = _las.prepare(scene, mask.view(torch.bool), c)
+        eligible, _, n_split, flags = (int(v) for v in torch.cat([counts, prep.summary]).cpu())
+        _las.check_and_apply(prep, n_split, flags, c)
+    else:
+        eligible, n_split = eligible_count(stats, cfg, step), 0
+    stats.reset(scene.count)
+    return DensifyEvent(step=step, eligible=eligible, split=n_split, count_after=scene.count)

@@ -1,0 +1,124 @@
+"""Drop-in for ``splitkit.las_split`` (3D batch path) on B200.
+
+``las_split_batch(scene, mask, c)`` keeps the reference contract
+(``/root/reference/pkg/src/splitkit/las_split.py:146-179``): masked parents are
+overwritten in place by their +offset child, the -offset children are appended
+in ascending parent order, ``BudgetError`` / ``ValueError`` are raised before
+anything is written, an all-false mask leaves the scene untouched.
+
+Device flow: ``igs_las_prepare`` (mask scan + batch flags) -> one 16-byte
+device->host read of {n_split, flags} -> host checks -> ``igs_las_apply``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import Scene3
+
+
+class BudgetError(RuntimeError):
+    """Raised when a split would push a scene past its capacity (las_split.py:26-27)."""
+
+
+@dataclass(frozen=True)
+class SplitConstants:
+    """Shrink/opacity factors applied to both children of a split (las_split.py:30-49)."""
+
+    alpha: float = 0.5
+    gamma_axis: float = 0.85
+    beta: float = 0.6
+
+    def __post_init__(self):
+        if not 0.0 < self.alpha < 1.0:
+            raise ValueError("alpha must be in (0, 1)")
+        if not 0.0 < self.gamma_axis <= 1.0:
+            raise ValueError("gamma_axis must be in (0, 1]")
+        if not 0.0 < self.beta <= 1.0:
+            raise ValueError("beta must be in (0, 1]")
+
+    def device_constants(self):
+        """float32 (alpha, log alpha, log gamma, beta) exactly as _split_common casts them."""
+        f = np.float32
+        return (float(f(self.alpha)), float(f(math.log(self.alpha))),
+                float(f(math.log(self.gamma_axis))), float(f(self.beta)))
+
+
+def _mask_tensor(mask, n, device):
+    if isinstance(mask, torch.Tensor):
+        m = mask.to(device)
+    else:
+        m = torch.from_numpy(np.ascontiguousarray(np.asarray(mask, dtype=bool))).to(device)
+    if tuple(m.shape) != (n,):
+        raise ValueError(f"mask length {tuple(m.shape)} does not match scene count {n}")
+    if m.dtype != torch.bool:
+        m = m != 0
+    return m.contiguous().view(torch.uint8)
+
+
+class _Prepared:
+    """Result of the device pre-pass (workspace stays bound until apply)."""
+
+    def __init__(self, scene, mask_u8, ws, summary):
+        self.scene, self.mask_u8, self.ws, self.summary = scene, mask_u8, ws, summary
+
+
+def prepare(scene: Scene3, mask, c: SplitConstants):
+    """Launch the pre-pass; returns a handle whose .summary (device int64[2]) is not yet read."""
+    L = _lib.lib()
+    m = _mask_tensor(mask, scene.count, scene.device)
+    nbytes = _lib.query_size(L.igs_las_workspace_bytes, scene.count)
+    ws = _lib.workspace(nbytes, scene.device, "las")
+    summary = torch.empty(2, dtype=torch.int64, device=scene.device)
+    _, _, _, beta = c.device_constants()
+    _lib.check(L.igs_las_prepare(m.data_ptr(), scene._rot.data_ptr(), scene._op.data_ptr(),
+                                 scene.count, beta, ws.data_ptr(), ws.numel(),
+                                 summary.data_ptr(), _lib.stream_handle()), "las_split_batch")
+    return _Prepared(scene, m, ws, summary)
+
+
+def check_and_apply(prep: _Prepared, n_split: int, flags: int, c: SplitConstants):
+    """Host checks in the reference's order, then the split pass.  Returns the new count."""
+    scene = prep.scene
+    if scene.count + n_split > scene.capacity:
+        raise BudgetError(f"splitting {n_split} of {scene.count} primitives exceeds "
+                          f"capacity {scene.capacity}")
+    if n_split == 0:
+        return scene.count
+    if flags & _lib.IGS_LAS_BAD_OPACITY:
+        raise ValueError("logit requires all values strictly inside (0, 1)")
+    if flags & _lib.IGS_LAS_BAD_QUAT:
+        raise ValueError("zero or non-finite quaternion")
+    L = _lib.lib()
+    alpha, log_alpha, log_gamma, beta = c.device_constants()
+    sh_floats = scene._sh.shape[1] * 3
+    _lib.check(L.igs_las_apply(scene._pos.data_ptr(), scene._ls.data_ptr(), scene._rot.data_ptr(),
+                               scene._op.data_ptr(), scene._sh.data_ptr(), sh_floats, scene.count,
+                               scene.capacity, prep.mask_u8.data_ptr(), alpha, log_alpha,
+                               log_gamma, beta, int(bool(flags & _lib.IGS_LAS_RENORM)),
+                               prep.ws.data_ptr(), prep.ws.numel(), _lib.stream_handle()),
+               "las_split_batch")
+    scene._set_count(scene.count + n_split)
+    return scene.count
+
+
+def las_split_batch(scene: Scene3, mask, c: SplitConstants = SplitConstants()) -> Scene3:
+    """Split every masked primitive of a GPU scene in place (las_split.py:158-179)."""
+    if not isinstance(scene, Scene3):
+        raise TypeError(f"expected a paper_2603_08661_b200.core.Scene3, got {type(scene).__name__}")
+    prep = prepare(scene, mask, c)
+    n_split, flags = (int(v) for v in prep.summary.cpu().tolist())
+    check_and_apply(prep, n_split, flags, c)
+    return scene.validate()
+
+
+def principal_axis(log_scale):
+    """Index of the largest log-scale, ties to the lowest index (las_split.py:52-59)."""
+    t = log_scale if isinstance(log_scale, torch.Tensor) else torch.as_tensor(np.asarray(log_scale))
+    idx = torch.argmax(t, dim=-1)
+    return int(idx) if idx.ndim == 0 else idx

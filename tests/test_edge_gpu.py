@@ -1,0 +1,182 @@
+"""Parity of the CUDA edge-importance path with the oracle and the reference's golden vectors."""
+
+import numpy as np
+import pytest
+import torch
+from numpy.testing import assert_allclose, assert_array_equal
+
+from conftest import load_golden
+from oracle import edge as OE
+
+pytestmark = pytest.mark.gpu
+
+EDGE = load_golden("edge")
+
+
+def B():
+    import paper_2603_08661_b200 as b
+    return b
+
+
+@pytest.mark.parametrize("case", sorted(EDGE))
+def test_golden_pipeline_bit_exact(case):
+    c = EDGE[case]
+    img, sigma = c["image"], float(c["sigma"])
+    if min(img.shape[:2]) < 3:
+        pytest.skip("pipeline needs >= 3x3")
+    got = B().importance_pipeline(img, sigma)
+    assert got.dtype == np.float64
+    assert_array_equal(got, c["importance"])
+
+
+@pytest.mark.parametrize("case", sorted(EDGE))
+def test_golden_stages(case):
+    b = B()
+    c = EDGE[case]
+    img, sigma = c["image"], float(c["sigma"])
+    if img.ndim == 3:
+        assert_array_equal(b.to_grayscale(img), c["gray"])
+    assert_array_equal(b.gaussian_blur_5x5(c["gray"], sigma), c["blurred"])
+    if min(img.shape[:2]) < 3:
+        return
+    f = b.sobel_gradients(c["blurred"])
+    assert_array_equal(f.magnitude, c["magnitude"])
+    # orientation lives on a circle of circumference pi (pkg/tests/test_edge_pipeline.py:155-158):
+    # CUDA's atan2 can land one ulp below pi where glibc rounds to pi (-> 0 after mod pi)
+    d = np.abs(f.orientation - c["orientation"])
+    assert (np.minimum(d, np.pi - d) <= 4e-15).all()
+    # NMS stage on the reference's own field: bit-exact
+    assert_array_equal(b.nms_thin(b.GradientField(c["magnitude"], c["orientation"])),
+                       c["thinned"])
+    # fused --no-median output == thinned map
+    assert_array_equal(b.importance_pipeline(img, sigma, median=False), c["thinned"])
+    assert_array_equal(b.importance_pipeline(img, sigma, nms=False, median=False),
+                       c["magnitude"])
+
+
+def test_nms_golden_fields():
+    b = B()
+    for name, c in load_golden("nms").items():
+        assert_array_equal(b.nms_thin(b.GradientField(c["mag"], c["ori"])), c["out"],
+                           err_msg=name)
+
+
+def test_median_golden():
+    b = B()
+    for name, c in load_golden("median").items():
+        assert_array_equal(b.median_normalize(c["in"]), c["out"], err_msg=name)
+
+
+def test_median_large_random_vs_oracle():
+    b = B()
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 3, 1000, 1001, 1_000_003):
+        for kind in ("uniform", "ties", "spread"):
+            if kind == "uniform":
+                a = rng.random(n) * (rng.random(n) > 0.4)
+            elif kind == "ties":
+                a = np.round(rng.random(n) * 5) / 5
+            else:
+                a = np.exp(rng.uniform(-200, 60, n)) * (rng.random(n) > 0.5)
+            assert_array_equal(b.median_normalize(a), OE.median_normalize(a), err_msg=f"{n} {kind}")
+
+
+def _views():
+    from paper_2603_08661_b200.synth import synth_view
+    rng = np.random.default_rng(9)
+    h, w = 822, 1237
+    views = [synth_view(h, w, 1000), synth_view(h, w, 1001)]
+    blocks = np.kron(rng.integers(0, 256, (52, 78, 3)), np.ones((16, 16, 1)))[:h, :w] / 255.0
+    rect = np.zeros((h, w, 3))
+    rect[100:500, 200:900] = 1.0
+    views += [blocks, rect, rng.random((h, w, 3))]
+    return np.stack(views)
+
+
+def test_full_size_views_batched_bit_exact():
+    b = B()
+    views = _views()
+    got = b.importance_batch(views)
+    for v in range(views.shape[0]):
+        want = OE.importance_pipeline(views[v])
+        diff = np.flatnonzero(got[v] != want)
+        assert diff.size == 0, f"view {v}: {diff.size} differing pixels"
+
+
+def test_full_size_nms_mask_and_magnitudes():
+    """Survivor masks bit-exact; magnitudes within 1e-5 relative (the north-star tolerance)."""
+    b = B()
+    views = _views()[:2]
+    got = b.importance_batch(views, median=False)
+    for v in range(2):
+        want = OE.importance_pipeline(views[v], median=False)
+        assert_array_equal(got[v] > 0, want > 0)
+        assert_allclose(got[v], want, rtol=1e-5, atol=0)
+
+
+def test_float32_input_and_gray_batch():
+    b = B()
+    views = _views()[:2]
+    v32 = views.astype(np.float32)
+    got = b.importance_batch(v32)
+    for v in range(2):
+        assert_array_equal(got[v], OE.importance_pipeline(v32[v]))
+    gray = np.stack([OE.to_grayscale(x) * 3 - 1 for x in views])   # not clipped on entry
+    got = b.importance_batch(gray)
+    for v in range(2):
+        assert_array_equal(got[v], OE.importance_pipeline(gray[v]))
+
+
+def test_odd_sizes_and_many_views():
+    b = B()
+    rng = np.random.default_rng(11)
+    for (h, w, n) in ((3, 3, 5), (3, 200, 3), (97, 5, 4), (61, 121, 11), (33, 64, 9)):
+        imgs = np.floor(rng.random((n, h, w, 3)) * 255) / 255
+        got = b.importance_batch(imgs)
+        for v in range(n):
+            assert_array_equal(got[v], OE.importance_pipeline(imgs[v]), err_msg=f"{h}x{w} v{v}")
+
+
+def test_torch_in_torch_out():
+    b = B()
+    img = torch.from_numpy(EDGE["synth"]["image"]).cuda()
+    out = b.importance_pipeline(img)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    assert_array_equal(out.cpu().numpy(), EDGE["synth"]["importance"])
+
+
+def test_errors():
+    b = B()
+    with pytest.raises(ValueError):
+        b.to_grayscale(np.zeros((4, 5)))
+    with pytest.raises(ValueError):
+        b.to_grayscale(np.zeros((4, 5, 4)))
+    with pytest.raises(ValueError):
+        b.sobel_gradients(np.zeros((2, 5)))
+    with pytest.raises(ValueError):
+        b.importance_pipeline(np.zeros((2, 5, 3)))
+    with pytest.raises(ValueError):
+        b.blur_kernel_5x5(0.0)
+    with pytest.raises(ValueError):
+        b.GradientField(np.zeros((3, 3)), np.zeros((3, 4)))
+
+
+def test_reference_known_answers():
+    """pkg/tests/test_edge_pipeline.py + acceptance criterion 4 on the CUDA path."""
+    b = B()
+    assert_allclose(b.to_grayscale(np.ones((4, 5, 3))), 1.0, atol=1e-6)
+    g = np.zeros((11, 11))
+    g[5, 5] = 1.0
+    assert_allclose(b.gaussian_blur_5x5(g, 1.0)[3:8, 3:8], b.blur_kernel_5x5(1.0), atol=1e-12)
+    step = np.full((10, 10), 0.2)
+    step[:, 5:] = 0.8
+    f = b.sobel_gradients(step)
+    assert_allclose(f.magnitude[:, 4:6], 2.4, atol=1e-12)
+    mag = np.zeros((3, 5))
+    mag[1, 1:4] = 0.7
+    assert_array_equal(b.nms_thin(b.GradientField(mag, np.zeros((3, 5))))[1], [0, .7, 0, 0, 0])
+    step = np.full((128, 128), 0.2)
+    step[:, 64:] = 0.8
+    thinned = b.importance_pipeline(step, median=False)
+    assert ((thinned[2:-2] > 1e-9).sum(axis=1) == 1).all()
+    assert_array_equal(b.importance_pipeline(np.zeros((16, 16, 3))), 0.0)

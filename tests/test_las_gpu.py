@@ -1,0 +1,160 @@
+"""Parity of the CUDA Long-Axis-Split with the oracle and the reference's golden vectors."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+from numpy.testing import assert_array_equal
+
+from conftest import load_golden
+from oracle import las as OL
+
+pytestmark = pytest.mark.gpu
+
+LAS = load_golden("las")
+
+
+def B():
+    import paper_2603_08661_b200 as b
+    return b
+
+
+def assert_las_close(got, want, label=""):
+    """rotations, SH and child log-scales bit-exact; positions within
+    1e-5 (|p| + |disp|); opacity within 1e-5 max(1, |o|)."""
+    for col in ("rotations", "log_scales", "sh"):
+        assert_array_equal(got[col], want[col], err_msg=f"{label} {col}")
+    gp, wp = got["positions"].astype(np.float64), want["positions"].astype(np.float64)
+    assert gp.shape == wp.shape, label
+    scale = np.abs(wp) + np.exp(want["log_scales"].astype(np.float64)).max(axis=1,
+                                                                           keepdims=True) * 2
+    assert (np.abs(gp - wp) <= 1e-5 * scale).all(), f"{label} positions"
+    go, wo = got["opacity_logits"].astype(np.float64), want["opacity_logits"].astype(np.float64)
+    assert (np.abs(go - wo) <= 1e-5 * np.maximum(1.0, np.abs(wo))).all(), f"{label} opacity"
+
+
+def scene_dict(c, prefix):
+    return {"positions": c[f"{prefix}_positions"], "log_scales": c[f"{prefix}_log_scales"],
+            "rotations": c[f"{prefix}_rotations"], "opacity_logits": c[f"{prefix}_opacity_logits"],
+            "sh": c[f"{prefix}_colors"][:, None, :], "capacity": int(c["capacity"])}
+
+
+def gpu_scene(d):
+    return B().Scene3(d["positions"], d["log_scales"], d["rotations"], d["opacity_logits"],
+                      d["sh"], d["capacity"])
+
+
+@pytest.mark.parametrize("case", sorted(LAS))
+def test_golden_las(case):
+    b = B()
+    c = LAS[case]
+    consts = b.SplitConstants(*c["constants"]) if "constants" in c else b.SplitConstants()
+    s = gpu_scene(scene_dict(c, "in"))
+    b.las_split_batch(s, c["mask"], consts)
+    assert s.count == len(c["out_positions"])
+    assert_las_close(s.to_numpy(), scene_dict(c, "out"), case)
+
+
+def test_sh_degree3_clone_vs_oracle():
+    b = B()
+    from paper_2603_08661_b200.synth import random_cloud
+    n = 20_000
+    pos, ls, q, o, sh = random_cloud(n, 16, seed=5)
+    rng = np.random.default_rng(6)
+    for p in (0.05, 0.5, 1.0):
+        mask = rng.random(n) < p
+        d = {"positions": pos, "log_scales": ls, "rotations": q, "opacity_logits": o, "sh": sh,
+             "capacity": 2 * n + 3}
+        want = OL.las_split_batch(d, mask)
+        s = gpu_scene(d)
+        b.las_split_batch(s, torch.from_numpy(mask).cuda())
+        assert_las_close(s.to_numpy(), want, f"p={p}")
+
+
+def test_million_all_masked_acceptance_ratios():
+    """Acceptance criterion 1 (test_acceptance.py:61-104) on 1M splits, plus oracle parity."""
+    b = B()
+    from paper_2603_08661_b200.synth import random_cloud
+    n = 1_000_000
+    pos, ls, q, o, sh = random_cloud(n, 16, seed=101)
+    d = {"positions": pos, "log_scales": ls, "rotations": q, "opacity_logits": o, "sh": sh,
+         "capacity": 2 * n}
+    s = gpu_scene(d)
+    b.las_split_batch(s, np.ones(n, bool))
+    got = s.to_numpy()
+    assert s.count == 2 * n
+    want = OL.las_split_batch(d, np.ones(n, bool))
+    assert_las_close(got, want, "1M")
+    first, second = slice(0, n), slice(n, 2 * n)
+    P = got["positions"].astype(np.float64)
+    mid = (P[first] + P[second]) / 2
+    assert np.abs(mid - pos).max() <= 1e-6 * 4   # float32 positions of magnitude ~4
+    ratios = np.exp(got["log_scales"][first].astype(np.float64) - ls.astype(np.float64))
+    la = np.argmax(ls, axis=1)
+    rows = np.arange(n)
+    assert np.abs(ratios[rows, la] / 0.5 - 1).max() <= 1e-6
+    other = np.ones((n, 3), bool)
+    other[rows, la] = False
+    assert np.abs(ratios[other] / 0.85 - 1).max() <= 1e-6
+    sig = lambda x: 1 / (1 + np.exp(-x.astype(np.float64)))
+    assert np.abs(sig(got["opacity_logits"][first]) / sig(o) - 0.6).max() <= 1e-6
+
+
+def test_errors_leave_scene_untouched():
+    b = B()
+    z = np.zeros((4, 3), np.float32)
+    q = np.tile(np.array([1, 0, 0, 0], np.float32), (4, 1))
+    s = b.Scene3(z, z, q, np.zeros(4, np.float32), np.ones((4, 3), np.float32), 5)
+    with pytest.raises(b.BudgetError):
+        b.las_split_batch(s, np.ones(4, bool))
+    with pytest.raises(ValueError):
+        b.las_split_batch(s, np.ones(3, bool))
+    s2 = b.Scene3(z, z, q, np.zeros(4, np.float32), np.ones((4, 3), np.float32), 8)
+    s2._rot[2] = 0.0
+    before = s2.to_numpy()
+    with pytest.raises(ValueError):
+        b.las_split_batch(s2, np.ones(4, bool))
+    after = s2.to_numpy()
+    assert s2.count == 4
+    for k in ("positions", "log_scales", "opacity_logits"):
+        assert_array_equal(after[k], before[k])
+    # logit domain: sigmoid(-100) underflows to 0 in float32 -> ValueError (core.py:27-28)
+    s3 = b.Scene3(z, z, q, np.array([0, -100, 0, 0], np.float32), np.ones((4, 3), np.float32), 8)
+    with pytest.raises(ValueError):
+        b.las_split_batch(s3, np.array([False, True, False, False]))
+    assert s3.count == 4
+    # the same parent unmasked is fine
+    b.las_split_batch(s3, np.array([True, False, False, False]))
+    assert s3.count == 5
+
+
+def test_empty_mask_and_worked_example():
+    b = B()
+    s = b.Scene3(np.zeros((1, 3)), np.zeros((1, 3)), [[1, 0, 0, 0]], [0.0], [[1, 1, 1]], 4)
+    b.las_split_batch(s, [False])
+    assert s.count == 1
+    b.las_split_batch(s, [True])
+    g = s.to_numpy()
+    np.testing.assert_allclose(g["positions"], [[0.5, 0, 0], [-0.5, 0, 0]], atol=1e-7)
+    np.testing.assert_allclose(g["log_scales"][0], [math.log(.5), math.log(.85), math.log(.85)],
+                               atol=1e-6)
+    np.testing.assert_allclose(g["opacity_logits"], -0.847298, atol=1e-6)
+
+
+def test_batch_equals_sequential_random_scenes():
+    """Acceptance criterion 3 (batch == sequential) via the oracle, 200 random scenes."""
+    b = B()
+    rng = np.random.default_rng(103)
+    for _ in range(200):
+        n = int(rng.integers(1, 300))
+        d = {"positions": rng.normal(0, 1, (n, 3)).astype(np.float32),
+             "log_scales": rng.uniform(-.7, .7, (n, 3)).astype(np.float32),
+             "rotations": (lambda q: (q / np.linalg.norm(q, axis=1, keepdims=True)))(
+                 rng.normal(size=(n, 4))).astype(np.float32),
+             "opacity_logits": rng.normal(0, 1.5, n).astype(np.float32),
+             "sh": rng.random((n, 1, 3)).astype(np.float32), "capacity": 2 * n + 1}
+        mask = rng.random(n) < 0.4
+        s = gpu_scene(d)
+        b.las_split_batch(s, mask)
+        assert_las_close(s.to_numpy(), OL.las_split_batch(d, mask))
