@@ -1,0 +1,409 @@
+"""Benchmark of the B200 densification hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline (N=1 workload = BASELINE.json configs[1]): edge-importance maps + per-view
+median normalisation over 200 synthetic 1237x822 RGB float64 views per GPU
+("edge-map MPix/s").  One step = one importance_batch() over the 200 resident views
+(one fused persistent kernel launch).  Inputs (4.9 GB) are far larger than L2, so
+no flush is needed between steps.  Secondary object "las": Long-Axis-Split of a 1M-
+Gaussian SH-degree-3 cloud (configs[2], all-masked bandwidth case) plus the full
+densify_step (select 50k of 1M + LAS).
+
+Multi-GPU (torchrun, one rank per GPU): views shard per GPU (weak scaling, no
+collective on the data path); value = all ranks' pixels / max-over-ranks time.
+
+--impl reference: the reference's CPU path on this host -- the oracle port of
+splitkit.edge_pipeline (numpy/scipy-order restatement, oracle/edge.py) over a pool of
+all host cores, one view per process per step; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, W = 822, 1237
+PX = H * W
+VIEWS = 200
+BYTES_PER_PX_F64 = 24 + 8          # f64 RGB in + f64 map out
+LAS_N = 1_000_000
+LAS_BYTES_PER_SPLIT = 236 + 28 + 236  # read record, in-place parent, appended child
+METRIC = "edge-map MPix/s"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """DRAM bytes per unit from the committed ncu capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms while active."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ CPU reference (oracle)
+_CPU_VIEW = None
+
+
+def _cpu_init(seed):
+    global _CPU_VIEW
+    from paper_2603_08661_b200.synth import synth_view
+    _CPU_VIEW = synth_view(H, W, seed + os.getpid() % 97)
+
+
+def _cpu_task(_):
+    from oracle import edge as OE
+    t0 = time.perf_counter()
+    OE.importance_pipeline(_CPU_VIEW)
+    return time.perf_counter() - t0
+
+
+def cpu_edge_rate(steps, warmup, procs=None):
+    """Oracle edge pipeline over a process pool (1 view per process per step) -> MPix/s."""
+    import multiprocessing as mp
+    procs = procs or len(os.sched_getaffinity(0))
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs, initializer=_cpu_init, initargs=(1000,)) as pool:
+        for _ in range(warmup):
+            pool.map(_cpu_task, range(procs), chunksize=1)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            pool.map(_cpu_task, range(procs), chunksize=1)
+        wall = time.perf_counter() - t0
+    return steps * procs * PX / wall / 1e6, procs, wall / steps
+
+
+def cpu_las_rate(n=200_000):
+    from oracle import las as OL
+    from paper_2603_08661_b200.synth import random_cloud
+    import numpy as np
+    pos, ls, q, o, sh = random_cloud(n, 16, seed=101)
+    d = {"positions": pos, "log_scales": ls, "rotations": q, "opacity_logits": o, "sh": sh,
+         "capacity": 2 * n}
+    mask = np.ones(n, bool)
+    OL.las_split_batch(d, mask)
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        OL.las_split_batch(d, mask)
+    return n * reps / (time.perf_counter() - t0)
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    steps = max(1, args.steps if args.steps_given else 5)
+    warmup = max(0, min(args.warmup, 2))
+    rate, procs, sec = cpu_edge_rate(steps, warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(rate, 3), "unit": "MPix/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "200 x 1237x822 RGB f64 views: gray+blur+Sobel+NMS+median "
+                               "(BASELINE.json configs[1])", "views_per_gpu": VIEWS,
+                   "height": H, "width": W},
+        "cpu_baseline": {"value": round(rate, 3), "unit": "MPix/s", "cores": procs, "kind": "port",
+                         "sample": f"{procs} views per step (1 per process), oracle/edge.py "
+                                   "numpy restatement of splitkit.edge_pipeline"},
+        "e2e": {"value": round(rate, 3), "unit": "MPix/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU (ours)
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2603_08661_b200 as igs
+    from paper_2603_08661_b200.synth import synth_views_torch
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    peak, peak_src = peaks()
+    views = synth_views_torch(VIEWS, H, W, seed=1000 + 17 * rank, device=dev)
+    out = torch.empty((VIEWS, H, W), dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        igs.importance_batch(views, out=out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            igs.importance_batch(views, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms, world)
+    value = world * VIEWS * PX / (ms * 1e-3) / 1e6
+    algo_bytes = VIEWS * PX * BYTES_PER_PX_F64
+    achieved = algo_bytes / (ms * 1e-3) / 1e9
+    traffic = ncu_traffic().get("edge_persistent_kernel_bytes_per_px")
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "MPix/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "200 x 1237x822 RGB f64 views per GPU: gray+blur+Sobel+NMS+"
+                               "median normalisation (BASELINE.json configs[1])",
+                   "views_per_gpu": VIEWS, "height": H, "width": W, "io": "f64 in / f64 out",
+                   "l2": "inputs 4.9 GB per GPU >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"views sharded, {world} GPU(s), no data-path collective"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": (round(traffic * VIEWS * PX) if traffic else None),
+                     "kernel": "edge_persistent_kernel", "algorithmic_bytes_per_px": 32,
+                     "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps,
+    }
+    if not args.no_e2e:
+        line["e2e"] = e2e_edge(args, world, dev)
+    if not args.no_las:
+        line["las"] = bench_las(args, world, dev, peak, peak_src)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, procs, _ = cpu_edge_rate(2, 1)
+        line["cpu_baseline"] = {"value": round(rate, 3), "unit": "MPix/s", "cores": procs,
+                                "kind": "port",
+                                "sample": f"3x{procs} views (1 per process per step), "
+                                          "oracle/edge.py on the host cores"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def e2e_edge(args, world, dev):
+    """Public API with host buffers: pinned (B,H,W,3) f64 in, pinned (B,H,W) f64 out; the H2D
+    of the inputs and the D2H of the maps are inside the timed region, every step."""
+    import torch
+
+    import paper_2603_08661_b200 as igs
+    from paper_2603_08661_b200.synth import synth_views_torch
+    host_in = synth_views_torch(VIEWS, H, W, seed=2000, device=dev).cpu().pin_memory()
+    host_out = torch.empty((VIEWS, H, W), dtype=torch.float64).pin_memory()
+    steps = max(2, min(args.steps, 5))
+    for _ in range(2):
+        igs.importance_batch(host_in, out=host_out)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        igs.importance_batch(host_in, out=host_out)   # returns after the D2H has landed
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / steps
+    barrier(world)
+    sec = max_over_ranks(sec, world)
+    return {"value": round(world * VIEWS * PX / sec / 1e6, 3), "unit": "MPix/s",
+            "h2d_bytes_per_step": VIEWS * PX * 24, "d2h_bytes_per_step": VIEWS * PX * 8,
+            "ms_per_step": round(sec * 1e3, 3), "steps": steps,
+            "api": "importance_batch(pinned host views, out=pinned host maps), 8-view chunks "
+                   "with H2D / kernel / D2H overlapped on three streams"}
+
+
+def bench_las(args, world, dev, peak, peak_src):
+    import torch
+
+    import paper_2603_08661_b200 as igs
+    from paper_2603_08661_b200 import _lib
+    from paper_2603_08661_b200.synth import random_cloud_torch, random_stats
+
+    n = LAS_N
+    pos, ls, q, o, sh = random_cloud_torch(n, 16, seed=101, device=dev)
+    scene = igs.Scene3(pos, ls, q, o, sh, capacity=2 * n, device=dev)
+    pristine = {k: getattr(scene, k).clone() for k in ("_pos", "_ls", "_op")}
+    mask = torch.ones(n, dtype=torch.bool, device=dev)
+
+    def restore():
+        for k, v in pristine.items():
+            getattr(scene, k)[:n].copy_(v[:n])
+        scene._set_count(n)
+
+    # all-masked LAS through the public call (prepare + 16-byte D2H + apply)
+    times, kern = [], []
+    steps = max(3, min(args.steps, 20))
+    for it in range(args.warmup + steps):
+        restore()
+        torch.cuda.synchronize()
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record()
+        prep = igs.las_split.prepare(scene, mask, igs.SplitConstants())
+        ns, fl = (int(v) for v in prep.summary.cpu())
+        b.record()
+        igs.las_split.check_and_apply(prep, ns, fl, igs.SplitConstants())
+        c.record()
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            times.append(a.elapsed_time(c))
+            kern.append(b.elapsed_time(c))
+    ms = max_over_ranks(statistics.median(times), world)
+    ms_apply = max_over_ranks(statistics.median(kern), world)
+    achieved = n * LAS_BYTES_PER_SPLIT / (ms_apply * 1e-3) / 1e9
+    # full densify_step on the same cloud: select (take = 5% = 50k) + LAS
+    grad, edge = random_stats(n, seed=7)
+    dsteps = []
+    for it in range(args.warmup + steps):
+        restore()
+        stats = igs.DensifyStats(n, device=dev)
+        stats._grad_sum.copy_(torch.from_numpy(grad))
+        stats._accum_count = 1
+        stats.set_edge_score(edge)
+        cfg = igs.DensifyConfig(budget=2 * n)
+        torch.cuda.synchronize()
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ev = igs.densify_step(scene, stats, cfg, 2000)
+        c.record()
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            dsteps.append(a.elapsed_time(c))
+    ds_ms = max_over_ranks(statistics.median(dsteps), world)
+    res = {"metric": "LAS Gaussians/s", "value": round(world * n / (ms * 1e-3), 1),
+           "unit": "Gaussians/s", "ms_per_step": round(ms, 4),
+           "config": {"workload": "las_split_batch, 1M Gaussians all masked, SH degree 3 "
+                                  "(59 fp32/Gaussian), capacity 2M (BASELINE.json configs[2])",
+                      "l2": "500 MB moved per step >> L2"},
+           "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                        "kernel": "las_apply_kernel", "algorithmic_bytes_per_split": 500,
+                        "apply_ms": round(ms_apply, 4), "peak_source": peak_src},
+           "densify_step": {"ms": round(ds_ms, 4), "n": n, "split": ev.split,
+                            "eligible": ev.eligible,
+                            "note": "select (radix top-k, take=ceil(0.05 N)) + LAS + one host "
+                                    "sync, public densify_step()"}}
+    if world == 1 and not args.no_cpu:
+        rate = cpu_las_rate()
+        res["cpu_baseline"] = {"value": round(rate, 1), "unit": "Gaussians/s", "cores": 1,
+                               "kind": "port", "sample": "3 x 200k all-masked, SH degree 3, "
+                                                         "oracle/las.py"}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-las", action="store_true")
+    args = ap.parse_args()
+    args.steps_given = args.steps is not None
+    if args.steps is None:
+        args.steps = 50
+    args.warmup = max(args.warmup, 0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, world, int(os.environ.get("RANK", "0")))
+        return
+    world, rank, local = dist_setup()
+    try:
+        run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -16,8 +16,9 @@
 //           statistic(s) -> median m (np.median: (a+b)/2 for an even count). (:124)
 //   A(v,c)  apply: out = min(v / (2 m), 1) in place.                   (:125)
 // Queue order per step s: E(s) tiles, C(s-LAG1) chunks, A(s-LAG2) chunks, so
-// at most LAG2+1 views' thinned maps are live and they stay L2-resident
-// between E, C and A (the final map is written back to HBM once).
+// at most LAG2+1 views' thinned maps are live; they are stored with an L2
+// evict_last policy (the input streams with evict_first), so E, C and A meet in
+// L2 and the final map is written back to HBM once.
 //
 // Arithmetic: float64 in scipy's order (see oracle/edge.py): taps summed in
 // row-major order from 0.0 with separately rounded multiply and add; glibc's
@@ -29,6 +30,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "igs_common.cuh"
 
 namespace igs {
@@ -39,15 +42,19 @@ constexpr int MH = TH + 2, MW = TW + 2;      // gradient magnitude region (NMS h
 constexpr int BH = TH + 4, BW = TW + 4;      // blurred region (Sobel halo 1)
 constexpr int GH = TH + 8, GW = TW + 8;      // gray region (blur halo 2)
 constexpr int NT = 256;                      // threads per block
+constexpr int NWARP = NT / 32;
 constexpr int SB = 9;                        // blur strip height: BW x (BH/SB) = 256 strips
 static_assert(BW * (BH / SB) == NT && BH % SB == 0, "blur strips must cover the block");
 static_assert(MH * MW <= GH * GW, "magnitude aliases the gray buffer");
+static_assert(GW <= 96, "phase A covers a row with three lanes per warp lane");
 
-constexpr int NB = 2048;                     // median histogram: 16 bins per octave
+constexpr int NB = 2048;                     // level-1 median histogram: 16 bins per octave
 constexpr int HIST_BASE = 14768;             // (bits>>48) of 2^-100; bins cover [2^-100, 2^28)
+constexpr int NB2 = 4096;                    // level-2 histogram: bits 47..36 inside a bin
 constexpr int CHUNK = 32768;                 // pixels per collect/apply task
-constexpr int LAG1 = 2, LAG2 = 3;            // queue lags of C and A behind E
-constexpr int RING = LAG2 + 3;               // candidate buffers in flight
+constexpr int LAG1 = 2, LAG2 = 4;            // queue lags of C and A behind E
+constexpr int RING = LAG2 + 3;               // candidate buffers / level-2 histograms in flight
+constexpr int SEL_CAP = (GH * GW + BH * BW); // doubles of smem the select may use
 
 enum Mode { MODE_FUSED = 0, MODE_MEDIAN_ONLY = 1 };
 
@@ -57,7 +64,7 @@ struct ViewCtl {            // per-view control block, zeroed before launch
   unsigned collect_done;    // C tasks finished
   unsigned select_done;     // 1 once denom is published
   unsigned cnt1, cnt2;      // candidate append counters (front / back)
-  int b1, b2;               // median bins of ranks k1, k2
+  int b1, b2;               // level-1 bins of ranks k1, k2
   unsigned long long r1, r2;// ranks within those bins
   unsigned long long npos;  // positive count
   double denom;             // 2 * median
@@ -89,22 +96,54 @@ struct Params {
   unsigned long long* queue;
   ViewCtl* ctl;
   unsigned* hist;           // (B, NB)
+  unsigned* hist2;          // (RING, 2, NB2)
   double* cand;             // (RING, npx)
 };
 
 struct __align__(16) Smem {
-  double g[GH * GW];        // gray, then gradient magnitude
-  double b[BH * BW];        // blurred
+  double g[GH * GW];        // gray, then gradient magnitude; select scratch
+  double b[BH * BW];        // blurred; select scratch (contiguous with g)
   uint8_t bin[TH * TW];     // NMS direction bins of the output tile
   unsigned hist[NB];
   unsigned warp_sums[32];
-  long long task;
-  int flag;
+  int task_kind, task_view, task_idx, flag;
   int ivals[4];
+  unsigned long long u64[2];
 };
 
-__device__ __forceinline__ int clampi(long long v, long long lo, long long hi) {
-  return (int)(v < lo ? lo : (v > hi ? hi : v));
+// ---- L2 cache policies (input streamed once: evict_first; thinned map: evict_last) ----
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_hint(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_hint(const float* a, unsigned long long pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return (double)v;
+}
+__device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_cg_hint(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ int clamp_i(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+__device__ __forceinline__ long long clampi(long long v, long long lo, long long hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
 }
 
 __device__ __forceinline__ int hist_bin(double v) {
@@ -112,43 +151,63 @@ __device__ __forceinline__ int hist_bin(double v) {
   return hb < 0 ? 0 : (hb >= NB ? NB - 1 : (int)hb);
 }
 
-__device__ __forceinline__ double load_px(const Params& p, long long idx) {
-  return p.in_f64 ? __ldg((const double*)p.img + idx) : (double)__ldg((const float*)p.img + idx);
+// ---------------------------------------------------------------- E: fused tile
+// Phase A: gray over the GH x GW region at clamped coordinates (mode="nearest").  Warp w
+// walks rows w, w+8, ...; lane l covers columns l, l+32, l+64.
+template <int CH, bool F64>
+__device__ __forceinline__ void phase_gray(const Params& p, Smem& s, int v, int y0, int x0,
+                                           unsigned long long pol) {
+  using T = typename std::conditional<F64, double, float>::type;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int H = (int)p.H, W = (int)p.W;
+  const T* img = (const T*)p.img + (long long)v * p.npx * CH;
+  int xo[3];
+  bool ok[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int c = lane + 32 * k;
+    ok[k] = c < GW;
+    xo[k] = clamp_i(x0 - 4 + c, 0, W - 1) * CH;
+  }
+#pragma unroll
+  for (int u = warp; u < GH; u += NWARP) {
+    const T* row = img + (long long)clamp_i(y0 - 4 + u, 0, H - 1) * W * CH;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (!ok[k]) continue;
+      double g;
+      if (CH == 3) {
+        const double r = ld_hint(row + xo[k], pol), gg = ld_hint(row + xo[k] + 1, pol),
+                     bb = ld_hint(row + xo[k] + 2, pol);
+        g = np_clip01_int(((0.299 * r) + (0.587 * gg)) + (0.114 * bb));
+      } else {
+        g = ld_hint(row + xo[k], pol);
+      }
+      s.g[u * GW + lane + 32 * k] = g;
+    }
+  }
 }
 
-// ---------------------------------------------------------------- E: fused tile
-template <bool FAST>
-__device__ void run_tile(const Params& p, Smem& s, int v, int t) {
+template <bool FAST, int CH, bool F64>
+__device__ void run_tile(const Params& p, Smem& s, int v, int t, unsigned long long pol_in,
+                         unsigned long long pol_mid) {
   const int tid = threadIdx.x;
-  const long long H = p.H, W = p.W;
+  const int H = (int)p.H, W = (int)p.W;
   const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
-  const long long y0 = (long long)ty * TH, x0 = (long long)tx * TW;
+  const int y0 = ty * TH, x0 = tx * TW;
   const long long vbase = (long long)v * p.npx;
 
-  // Phase A: gray over the GH x GW region, stored at clamped coordinates (mode="nearest").
-  for (int i = tid; i < GH * GW; i += NT) {
-    int u = i / GW, c = i - u * GW;
-    int y = clampi(y0 - 4 + u, 0, H - 1), x = clampi(x0 - 4 + c, 0, W - 1);
-    long long pix = vbase + (long long)y * W + x;
-    double g;
-    if (p.channels == 3) {
-      double r = load_px(p, pix * 3), gg = load_px(p, pix * 3 + 1), bb = load_px(p, pix * 3 + 2);
-      g = np_clip01(((0.299 * r) + (0.587 * gg)) + (0.114 * bb));
-    } else {
-      g = load_px(p, pix);
-    }
-    s.g[i] = g;
-  }
+  phase_gray<CH, F64>(p, s, v, y0, x0, pol_in);
   __syncthreads();
 
-  // Phase B: 5x5 blur in vertical strips of SB outputs per thread.  Input rows stream
-  // top to bottom, so every output still accumulates its taps in row-major order.  With
-  // dihedrally symmetric weights (FAST) rows r-o and r-(4-o) share one product.
+  // Phase B: 5x5 blur in vertical strips of SB outputs per thread.  Input rows stream top
+  // to bottom, so every output accumulates its taps in NI_Correlate's row-major order.  With
+  // dihedrally symmetric weights (FAST) the products of rows r-o and r-(4-o) are shared.
+  // Each sum starts from its first product: identical to 0.0 + p except for the sign of an
+  // all-zero sum, which the clip maps to +0 either way.
   {
     const int c = tid % BW, u0 = (tid / BW) * SB;
     double acc[SB];
-#pragma unroll
-    for (int o = 0; o < SB; ++o) acc[o] = 0.0;
 #pragma unroll
     for (int r = 0; r < SB + 4; ++r) {
       double xv[5];
@@ -162,15 +221,17 @@ __device__ void run_tile(const Params& p, Smem& s, int v, int t) {
         for (int dj = 0; dj < 5; ++dj) {
           const int t25 = di * 5 + dj;
           if (FAST) {
-            acc[o] = acc[o] + xv[dj] * p.w6[di < 2 ? 2 - di : di - 2][dj < 2 ? 2 - dj : dj - 2];
-          } else if ((p.keep_mask >> t25) & 1u) {
-            acc[o] = acc[o] + xv[dj] * p.w25[t25];
+            const double prod = xv[dj] * p.w6[di < 2 ? 2 - di : di - 2][dj < 2 ? 2 - dj : dj - 2];
+            acc[o] = (t25 == 0) ? prod : acc[o] + prod;
+          } else {
+            if (t25 == 0) acc[o] = 0.0;
+            if ((p.keep_mask >> t25) & 1u) acc[o] = acc[o] + xv[dj] * p.w25[t25];
           }
         }
       }
     }
 #pragma unroll
-    for (int o = 0; o < SB; ++o) s.b[(u0 + o) * BW + c] = np_clip01(acc[o]);
+    for (int o = 0; o < SB; ++o) s.b[(u0 + o) * BW + c] = np_clip01_int(acc[o]);
   }
   __syncthreads();
   // Border tiles: out-of-image blurred cells take the value of the clamped in-image cell.
@@ -181,11 +242,11 @@ __device__ void run_tile(const Params& p, Smem& s, int v, int t) {
     bool fix[FIX];
 #pragma unroll
     for (int k = 0; k < FIX; ++k) {
-      int i = tid + k * NT, u = i / BW, c = i - u * BW;
-      long long y = y0 - 2 + u, x = x0 - 2 + c;
-      long long cy = y < 0 ? 0 : (y >= H ? H - 1 : y), cx = x < 0 ? 0 : (x >= W ? W - 1 : x);
+      const int i = tid + k * NT, u = i / BW, c = i - u * BW;
+      const int y = y0 - 2 + u, x = x0 - 2 + c;
+      const int cy = clamp_i(y, 0, H - 1), cx = clamp_i(x, 0, W - 1);
       fix[k] = (cy != y) || (cx != x);
-      val[k] = fix[k] ? s.b[(int)(cy - (y0 - 2)) * BW + (int)(cx - (x0 - 2))] : 0.0;
+      val[k] = fix[k] ? s.b[(cy - (y0 - 2)) * BW + (cx - (x0 - 2))] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -194,31 +255,28 @@ __device__ void run_tile(const Params& p, Smem& s, int v, int t) {
     __syncthreads();
   }
 
-  // Phase C: Sobel (NI_Correlate tap order, zero taps skipped), glibc hypot, direction bin.
+  // Phase C: Sobel (NI_Correlate tap order; the zero taps are skipped as scipy does; the
+  // exact x2 taps as FMAs), glibc hypot, direction bin of the output pixels.
   for (int i = tid; i < MH * MW; i += NT) {
-    int u = i / MW, c = i - u * MW;
-    long long y = y0 - 1 + u, x = x0 - 1 + c;
+    const int u = i / MW, c = i - u * MW;
+    const int y = y0 - 1 + u, x = x0 - 1 + c;
     double m = 0.0;  // out-of-image neighbours count as 0 for NMS (edge_pipeline.py:97)
     if (y >= 0 && y < H && x >= 0 && x < W) {
       const double* b = &s.b[u * BW + c];
-      double b00 = b[0], b01 = b[1], b02 = b[2];
-      double b10 = b[BW], b12 = b[BW + 2];
-      double b20 = b[2 * BW], b21 = b[2 * BW + 1], b22 = b[2 * BW + 2];
-      double gx = 0.0;
-      gx = gx + b00 * -1.0;
-      gx = gx + b02 * 1.0;
-      gx = gx + b10 * -2.0;
-      gx = gx + b12 * 2.0;
-      gx = gx + b20 * -1.0;
-      gx = gx + b22 * 1.0;
-      double gy = 0.0;
-      gy = gy + b00 * -1.0;
-      gy = gy + b01 * -2.0;
-      gy = gy + b02 * -1.0;
-      gy = gy + b20 * 1.0;
-      gy = gy + b21 * 2.0;
-      gy = gy + b22 * 1.0;
-      m = hypot_glibc(gx, gy);
+      const double b00 = b[0], b01 = b[1], b02 = b[2];
+      const double b10 = b[BW], b12 = b[BW + 2];
+      const double b20 = b[2 * BW], b21 = b[2 * BW + 1], b22 = b[2 * BW + 2];
+      double gx = b02 - b00;              // (0 + -b00) + b02
+      gx = fma(-2.0, b10, gx);
+      gx = fma(2.0, b12, gx);
+      gx = gx - b20;
+      gx = gx + b22;
+      double gy = fma(-2.0, b01, -b00);   // (0 + -b00) + -2 b01
+      gy = gy - b02;
+      gy = gy + b20;
+      gy = fma(2.0, b21, gy);
+      gy = gy + b22;
+      m = hypot_glibc_fast(gx, gy);
       if (p.nms && u >= 1 && u <= TH && c >= 1 && c <= TW)
         s.bin[(u - 1) * TW + (c - 1)] = (uint8_t)gradient_bin(gx, gy);
     }
@@ -226,25 +284,30 @@ __device__ void run_tile(const Params& p, Smem& s, int v, int t) {
   }
   __syncthreads();
 
-  // Phase D: NMS (keep iff m > prev and m >= next), store, histogram the survivors.
+  // Phase D: NMS (keep iff m > prev and m >= next; magnitudes are >= +0 or NaN, so the
+  // comparisons run on the bit patterns), store with L2 evict_last, histogram survivors.
   for (int i = tid; i < TH * TW; i += NT) {
-    int a = i / TW, c = i - a * TW;
-    long long y = y0 + a, x = x0 + c;
+    const int a = i / TW, c = i - a * TW;
+    const int y = y0 + a, x = x0 + c;
     if (y >= H || x >= W) continue;
     const double* mp = &s.g[(a + 1) * MW + (c + 1)];
-    double m = *mp, outv = m;
+    const double m = *mp;
+    double outv = m;
     if (p.nms) {
-      int bn = s.bin[i];
-      int po = bn == 0 ? -1 : (bn == 1 ? -MW - 1 : (bn == 2 ? -MW : -MW + 1));
-      bool keep = (m > mp[po]) && (m >= mp[-po]);
+      const int bn = s.bin[i];
+      const int po = bn == 0 ? -1 : (bn == 1 ? -MW - 1 : (bn == 2 ? -MW : -MW + 1));
+      const long long mb = __double_as_longlong(m);
+      const bool keep = (mb <= 0x7ff0000000000000LL) &&
+                        (mb > __double_as_longlong(mp[po])) &&
+                        (mb >= __double_as_longlong(mp[-po]));
       outv = keep ? m : 0.0;
     }
-    p.out[vbase + y * W + x] = outv;
+    st_hint(p.out + vbase + (long long)y * W + x, outv, pol_mid);
     if (p.median && outv > 0.0) atomicAdd(&s.hist[hist_bin(outv)], 1u);
   }
 }
 
-// ------------------------------------------------ histogram-only tile (median-only mode)
+// ------------------------------------------------ histogram-only chunk (median-only mode)
 __device__ void run_hist_chunk(const Params& p, Smem& s, int v, int c) {
   const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
   const double* src = (const double*)p.img + (long long)v * p.npx;
@@ -267,18 +330,49 @@ __device__ void flush_hist(const Params& p, Smem& s, int v) {
   }
 }
 
-// Last E task of a view: locate the bins holding ranks k1 = (n-1)/2 and k2 = n/2.
+// Locate the bin holding rank `rank` in a histogram of nb bins (nb % NT == 0, <= 16 * NT).
+// Every thread returns the same (bin, rank within bin) via smem.
+template <int NBINS>
+__device__ void locate(const unsigned* h, Smem& s, unsigned long long rank, int& bin,
+                       unsigned long long& rin, bool global_mem) {
+  constexpr int PER = NBINS / NT;
+  unsigned loc[PER], sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    loc[k] = global_mem ? __ldcg(&h[threadIdx.x * PER + k]) : h[threadIdx.x * PER + k];
+    sum += loc[k];
+  }
+  unsigned total;
+  unsigned before = block_exclusive_scan(sum, s.warp_sums, &total);
+  unsigned long long cum = before;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    if (loc[k] && rank >= cum && rank < cum + loc[k]) {
+      s.ivals[0] = threadIdx.x * PER + k;
+      s.u64[0] = rank - cum;
+    }
+    cum += loc[k];
+  }
+  __syncthreads();
+  bin = s.ivals[0];
+  rin = s.u64[0];
+  __syncthreads();
+}
+
+// Last E task of a view: locate the level-1 bins holding ranks k1 = (n-1)/2 and k2 = n/2.
 __device__ void find_median_bins(const Params& p, Smem& s, int v) {
   const unsigned* gh = p.hist + (long long)v * NB;
   constexpr int PER = NB / NT;
-  unsigned h[PER], local = 0;
+  unsigned local = 0;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    h[k] = __ldcg(&gh[threadIdx.x * PER + k]);
-    local += h[k];
-  }
-  unsigned total;
-  unsigned before = block_exclusive_scan(local, s.warp_sums, &total);
+  for (int k = 0; k < PER; ++k) local += __ldcg(&gh[threadIdx.x * PER + k]);
+  unsigned total = __reduce_add_sync(0xffffffffu, local);
+  if ((threadIdx.x & 31) == 0) s.warp_sums[threadIdx.x >> 5] = total;
+  __syncthreads();
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < NWARP; ++w) total += s.warp_sums[w];
+  __syncthreads();
   ViewCtl& ctl = p.ctl[v];
   if (total == 0) {
     if (threadIdx.x == 0) {
@@ -288,22 +382,17 @@ __device__ void find_median_bins(const Params& p, Smem& s, int v) {
       if (p.medians) p.medians[v] = 1.0;
     }
   } else {
-    const unsigned long long k1 = (total - 1) / 2, k2 = total / 2;
-    unsigned long long cum = before;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const unsigned long long nxt = cum + h[k];
-      if (h[k] && k1 >= cum && k1 < nxt) {
-        ctl.b1 = threadIdx.x * PER + k;
-        ctl.r1 = k1 - cum;
-      }
-      if (h[k] && k2 >= cum && k2 < nxt) {
-        ctl.b2 = threadIdx.x * PER + k;
-        ctl.r2 = k2 - cum;
-      }
-      cum = nxt;
+    int b1, b2;
+    unsigned long long r1, r2;
+    locate<NB>(gh, s, (total - 1) / 2, b1, r1, true);
+    locate<NB>(gh, s, total / 2, b2, r2, true);
+    if (threadIdx.x == 0) {
+      ctl.npos = total;
+      ctl.b1 = b1;
+      ctl.r1 = r1;
+      ctl.b2 = b2;
+      ctl.r2 = r2;
     }
-    if (threadIdx.x == 0) ctl.npos = total;
   }
   __threadfence();
   __syncthreads();
@@ -313,8 +402,24 @@ __device__ void find_median_bins(const Params& p, Smem& s, int v) {
   }
 }
 
+__device__ __forceinline__ int sub_bin(unsigned long long bits) { return (int)((bits >> 36) & (NB2 - 1)); }
+
 // ------------------------------------------------------------- C: collect candidates
-__device__ void run_collect(const Params& p, Smem& s, int v, int c) {
+__device__ void append(double x, bool f, unsigned* counter, double* base, int dir,
+                       unsigned* h2) {
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  if (!m) return;
+  unsigned slot = 0;
+  const int leader = __ffs(m) - 1;
+  if ((int)lane_id() == leader) slot = atomicAdd(counter, __popc(m));
+  slot = __shfl_sync(0xffffffffu, slot, leader);
+  if (f) {
+    base[dir * (long long)(slot + __popc(m & lanemask_lt()))] = x;
+    atomicAdd(&h2[sub_bin((unsigned long long)__double_as_longlong(x))], 1u);
+  }
+}
+
+__device__ void run_collect(const Params& p, Smem& s, int v, int c, unsigned long long pol_mid) {
   ViewCtl& ctl = p.ctl[v];
   if (threadIdx.x == 0) {
     spin_until_geq(&ctl.binfound, 1u);
@@ -324,125 +429,153 @@ __device__ void run_collect(const Params& p, Smem& s, int v, int c) {
     s.ivals[2] = __ldcg(&ctl.b2);
   }
   __syncthreads();
-  if (s.ivals[0]) {
-    const int b1 = s.ivals[1], b2 = s.ivals[2];
-    const double* src = (p.mode == MODE_FUSED) ? p.out + (long long)v * p.npx
-                                               : (const double*)p.img + (long long)v * p.npx;
-    double* cand = p.cand + (long long)(v % RING) * p.npx;
-    const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
-    for (long long base = lo; base < hi; base += NT) {
-      long long i = base + threadIdx.x;
-      double x = 0.0;
-      if (i < hi) x = __ldcg(src + i);
-      int hb = x > 0.0 ? hist_bin(x) : -1;
-      bool f1 = hb == b1, f2 = (hb == b2) && (b2 != b1);
-      unsigned m1 = __ballot_sync(0xffffffffu, f1), m2 = __ballot_sync(0xffffffffu, f2);
-      if (m1) {
-        unsigned slot = 0;
-        int leader = __ffs(m1) - 1;
-        if ((int)lane_id() == leader) slot = atomicAdd(&ctl.cnt1, __popc(m1));
-        slot = __shfl_sync(0xffffffffu, slot, leader);
-        if (f1) cand[slot + __popc(m1 & lanemask_lt())] = x;
-      }
-      if (m2) {
-        unsigned slot = 0;
-        int leader = __ffs(m2) - 1;
-        if ((int)lane_id() == leader) slot = atomicAdd(&ctl.cnt2, __popc(m2));
-        slot = __shfl_sync(0xffffffffu, slot, leader);
-        if (f2) cand[p.npx - 1 - (slot + __popc(m2 & lanemask_lt()))] = x;
-      }
+  if (!s.ivals[0]) return;
+  const int b1 = s.ivals[1], b2 = s.ivals[2];
+  const double* src = (p.mode == MODE_FUSED) ? p.out + (long long)v * p.npx
+                                             : (const double*)p.img + (long long)v * p.npx;
+  const int slot = v % RING;
+  double* cand = p.cand + (long long)slot * p.npx;
+  unsigned* h2a = p.hist2 + (long long)slot * 2 * NB2;
+  unsigned* h2b = h2a + NB2;
+  const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
+  constexpr int U = 8;
+  for (long long base = lo; base < hi; base += NT * U) {
+    double x[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = base + k * NT + threadIdx.x;
+      x[k] = i < hi ? ld_cg_hint(src + i, pol_mid) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int hb = x[k] > 0.0 ? hist_bin(x[k]) : -1;
+      append(x[k], hb == b1, &ctl.cnt1, cand, 1, h2a);
+      if (b2 != b1) append(x[k], hb == b2, &ctl.cnt2, cand + p.npx - 1, -1, h2b);
     }
   }
 }
 
-// Block-wide radix select: bits of the rank-th smallest among cand[0..n) (positive doubles,
-// so unsigned bit order == value order).  `dir` -1 reads the array backwards from `cand`.
-__device__ unsigned long long block_radix_select(Smem& s, const double* cand, long long n,
-                                                 int dir, unsigned long long rank) {
-  unsigned long long prefix = 0, pmask = 0;
-  unsigned* h = s.hist;  // reuse (cleared on entry and exit)
-  for (int pass = 0; pass < 6; ++pass) {
-    const int shift = pass < 5 ? 53 - 11 * pass : 0;
-    const unsigned dmask = pass < 5 ? 2047u : 511u;
-    const int nb = 2048;
-    for (int i = threadIdx.x; i < nb; i += NT) h[i] = 0;
+// Block-wide radix select over n positive doubles (bit order == value order) stored at
+// src[dir * i] (global or shared).  Bits above `top` are already known to be equal.
+__device__ unsigned long long block_radix_select(Smem& s, const double* src, long long n, int dir,
+                                                 unsigned long long rank, int top, bool global_mem) {
+  unsigned long long prefix = 0, pmask = top >= 63 ? 0ull : (~0ull << (top + 1));
+  unsigned* h = s.hist;  // reused; cleared on exit
+  if (n > 0 && pmask) {
+    double x0 = global_mem ? __ldcg(src) : src[0];
+    prefix = (unsigned long long)__double_as_longlong(x0) & pmask;
+  }
+  for (int hb = top; hb >= 0; hb -= 11) {
+    const int width = hb + 1 < 11 ? hb + 1 : 11;
+    const int shift = hb + 1 - width;
+    const unsigned dmask = (1u << width) - 1;
+    for (int i = threadIdx.x; i < NB; i += NT) h[i] = 0;
     __syncthreads();
     for (long long i = threadIdx.x; i < n; i += NT) {
-      unsigned long long bits = (unsigned long long)__double_as_longlong(__ldcg(cand + dir * i));
+      const double x = global_mem ? __ldcg(src + dir * i) : src[dir * i];
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
       if ((bits & pmask) == prefix) atomicAdd(&h[(bits >> shift) & dmask], 1u);
     }
     __syncthreads();
-    // find the digit: thread k owns bins [8k, 8k+8)
-    unsigned loc[8], sum = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      loc[k] = h[threadIdx.x * 8 + k];
-      sum += loc[k];
-    }
-    unsigned total;
-    unsigned before = block_exclusive_scan(sum, s.warp_sums, &total);
-    unsigned long long cum = before;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (loc[k] && rank >= cum && rank < cum + loc[k]) {
-        s.ivals[0] = threadIdx.x * 8 + k;
-        s.ivals[1] = (int)(rank - cum);
-      }
-      cum += loc[k];
-    }
-    __syncthreads();
-    const unsigned long long d = (unsigned)s.ivals[0];
-    rank = (unsigned)s.ivals[1];
-    prefix |= d << shift;
+    int d;
+    unsigned long long r;
+    locate<NB>(h, s, rank, d, r, false);
+    rank = r;
+    prefix |= (unsigned long long)d << shift;
     pmask |= (unsigned long long)dmask << shift;
-    __syncthreads();
   }
-  for (int i = threadIdx.x; i < NB; i += NT) s.hist[i] = 0;
+  for (int i = threadIdx.x; i < NB; i += NT) h[i] = 0;
   __syncthreads();
   return prefix;
 }
 
+// Order statistic `rank` of the candidates of level-1 bin b (region src[dir*i], i < n) whose
+// level-2 histogram is h2: locate the level-2 bin, stage its members in shared memory and
+// radix-select the low 36 bits there.  Clamped bins (0, NB-1) and oversize level-2 bins fall
+// back to a full-width select over the whole candidate list.
+__device__ double select_in_bin(Smem& s, const double* src, long long n, int dir, int b,
+                                unsigned long long rank, const unsigned* h2) {
+  if (b == 0 || b == NB - 1)
+    return __longlong_as_double(block_radix_select(s, src, n, dir, rank, 63, true));
+  int sb;
+  unsigned long long r2;
+  locate<NB2>(h2, s, rank, sb, r2, true);
+  const unsigned cnt = __ldcg(&h2[sb]);
+  if (cnt > (unsigned)SEL_CAP)
+    return __longlong_as_double(block_radix_select(s, src, n, dir, rank, 63, true));
+  double* buf = s.g;  // g and b are contiguous: SEL_CAP doubles
+  if (threadIdx.x == 0) s.ivals[1] = 0;
+  __syncthreads();
+  for (long long i = threadIdx.x; i < n; i += NT) {
+    const double x = __ldcg(src + dir * i);
+    if (sub_bin((unsigned long long)__double_as_longlong(x)) == sb) {
+      const int k = atomicAdd(&s.ivals[1], 1);
+      buf[k] = x;
+    }
+  }
+  __syncthreads();
+  return __longlong_as_double(block_radix_select(s, buf, cnt, 1, r2, 35, false));
+}
+
 __device__ void run_select(const Params& p, Smem& s, int v) {
   ViewCtl& ctl = p.ctl[v];
-  const double* cand = p.cand + (long long)(v % RING) * p.npx;
+  const int slot = v % RING;
+  const double* cand = p.cand + (long long)slot * p.npx;
+  unsigned* h2a = p.hist2 + (long long)slot * 2 * NB2;
+  unsigned* h2b = h2a + NB2;
   const unsigned n1 = __ldcg(&ctl.cnt1), n2 = __ldcg(&ctl.cnt2);
   const unsigned long long r1 = __ldcg(&ctl.r1), r2 = __ldcg(&ctl.r2);
   const int b1 = __ldcg(&ctl.b1), b2 = __ldcg(&ctl.b2);
-  double a = __longlong_as_double(block_radix_select(s, cand, n1, 1, r1));
-  double m = a;
   const unsigned long long npos = __ldcg(&ctl.npos);
+  const double a = select_in_bin(s, cand, n1, 1, b1, r1, h2a);
+  double m = a;
   if ((npos & 1ull) == 0) {
-    double b = (b2 == b1) ? __longlong_as_double(block_radix_select(s, cand, n1, 1, r2))
-                          : __longlong_as_double(
-                                block_radix_select(s, cand + p.npx - 1, n2, -1, r2));
+    const double b = (b2 == b1) ? select_in_bin(s, cand, n1, 1, b1, r2, h2a)
+                                : select_in_bin(s, cand + p.npx - 1, n2, -1, b2, r2, h2b);
     m = (a + b) / 2.0;
   }
+  // clear this slot's level-2 histograms for view v + RING
+  for (int i = threadIdx.x; i < 2 * NB2; i += NT) h2a[i] = 0;
   if (threadIdx.x == 0) {
     ctl.median = m;
     ctl.denom = 2.0 * m;
     if (p.medians) p.medians[v] = m;
-    __threadfence();
-    atomicExch(&ctl.select_done, 1u);
   }
+  __threadfence();
   __syncthreads();
+  if (threadIdx.x == 0) atomicExch(&ctl.select_done, 1u);
 }
 
 // ------------------------------------------------------------------ A: apply
-__device__ void run_apply(const Params& p, Smem& s, int v, int c) {
+__device__ void run_apply(const Params& p, Smem& s, int v, int c, unsigned long long pol_out) {
   ViewCtl& ctl = p.ctl[v];
-  if (threadIdx.x == 0) {
-    spin_until_geq(&ctl.select_done, 1u);
-    s.ivals[0] = 0;
-  }
+  if (threadIdx.x == 0) spin_until_geq(&ctl.select_done, 1u);
   __syncthreads();
   const double denom = __ldcg(&ctl.denom);
+  const double rd = __drcp_rn(denom);
   const double* src = (p.mode == MODE_FUSED) ? p.out + (long long)v * p.npx
                                              : (const double*)p.img + (long long)v * p.npx;
   double* dst = p.out + (long long)v * p.npx;
   const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
-  for (long long i = lo + threadIdx.x; i < hi; i += NT) {
-    double x = __ldcg(src + i);
-    __stcs(dst + i, np_min1(x / denom));
+  constexpr int U = 8;
+  const bool plain = isfinite(denom) && denom > 0x1p-1000 && denom < 0x1p+1000;
+  for (long long base = lo; base < hi; base += NT * U) {
+    double x[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = base + k * NT + threadIdx.x;
+      x[k] = i < hi ? __ldcg(src + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = base + k * NT + threadIdx.x;
+      if (i >= hi) continue;
+      double q;
+      if (x[k] == 0.0 && plain) q = 0.0 * rd;        // +-0 / denom, sign kept
+      else if (plain && fabs(x[k]) < 0x1p+900 && fabs(x[k]) > 0x1p-900) q = div_by(x[k], denom, rd);
+      else q = x[k] / denom;
+      st_hint(dst + i, np_min1(q), pol_out);
+    }
   }
 }
 
@@ -455,74 +588,95 @@ __device__ __forceinline__ long long step_start(const Params& p, long long st) {
          (long long)p.TA * clampll(st - LAG2, 0, p.B);
 }
 
-template <bool FAST>
-__global__ void __launch_bounds__(NT) edge_persistent_kernel(Params p) {
+enum TaskKind { TASK_END = 0, TASK_E = 1, TASK_C = 2, TASK_A = 3 };
+
+// Thread 0: decode queue index t into (kind, view, index).
+__device__ void decode_task(const Params& p, long long t, int& kind, int& view, int& idx) {
+  if (t >= p.total_tasks) {
+    kind = TASK_END;
+    return;
+  }
+  long long lo = 0, hi = p.B + (p.median ? LAG2 : 0);  // step_start(hi) > t
+  while (hi - lo > 1) {
+    const long long mid = (lo + hi) >> 1;
+    if (step_start(p, mid) <= t) lo = mid; else hi = mid;
+  }
+  long long off = t - step_start(p, lo);
+  const long long st = lo;
+  if (st < p.B) {
+    if (off < p.TE) {
+      kind = TASK_E; view = (int)st; idx = (int)off;
+      return;
+    }
+    off -= p.TE;
+  }
+  if (st >= LAG1 && st < p.B + LAG1) {
+    if (off < p.TC) {
+      kind = TASK_C; view = (int)(st - LAG1); idx = (int)off;
+      return;
+    }
+    off -= p.TC;
+  }
+  kind = TASK_A; view = (int)(st - LAG2); idx = (int)off;
+}
+
+template <bool FAST, int CH, bool F64>
+__global__ void __launch_bounds__(NT, 4) edge_persistent_kernel(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   for (int i = threadIdx.x; i < NB; i += NT) s.hist[i] = 0;
+  const unsigned long long pol_in = policy_evict_first();
+  const unsigned long long pol_mid = policy_evict_last();
+  const unsigned long long pol_out = policy_evict_first();
   __syncthreads();
-  const long long nsteps = p.B + (p.median ? LAG2 : 0);
   for (;;) {
-    if (threadIdx.x == 0) s.task = (long long)atomicAdd(p.queue, 1ull);
-    __syncthreads();
-    const long long t = s.task;
-    __syncthreads();
-    if (t >= p.total_tasks) break;
-    // locate the step: largest st with step_start(st) <= t
-    long long lo = 0, hi = nsteps;  // step_start(hi) > t
-    while (hi - lo > 1) {
-      long long mid = (lo + hi) >> 1;
-      if (step_start(p, mid) <= t) lo = mid; else hi = mid;
+    if (threadIdx.x == 0) {
+      int kind = 0, view = 0, idx = 0;
+      decode_task(p, (long long)atomicAdd(p.queue, 1ull), kind, view, idx);
+      s.task_kind = kind;
+      s.task_view = view;
+      s.task_idx = idx;
     }
-    long long off = t - step_start(p, lo);
-    const long long st = lo;
-    if (st < p.B) {
-      if (off < p.TE) {
-        const int v = (int)st;
-        if (p.mode == MODE_FUSED) run_tile<FAST>(p, s, v, (int)off);
-        else run_hist_chunk(p, s, v, (int)off);
-        if (p.median) {
-          flush_hist(p, s, v);
-          __threadfence();
-          __syncthreads();
-          if (threadIdx.x == 0) s.flag = (atomicAdd(&p.ctl[v].tiles_done, 1u) == (unsigned)p.TE - 1);
-          __syncthreads();
-          if (s.flag) {
-            __threadfence();
-            find_median_bins(p, s, v);
-          }
-        }
-        __syncthreads();
-        continue;
-      }
-      off -= p.TE;
-    }
-    if (st >= LAG1 && st < p.B + LAG1) {
-      if (off < p.TC) {
-        const int v = (int)(st - LAG1);
-        run_collect(p, s, v, (int)off);
+    __syncthreads();
+    const int kind = s.task_kind, v = s.task_view, idx = s.task_idx;
+    __syncthreads();
+    if (kind == TASK_END) break;
+    if (kind == TASK_E) {
+      if (p.mode == MODE_FUSED) run_tile<FAST, CH, F64>(p, s, v, idx, pol_in, pol_mid);
+      else run_hist_chunk(p, s, v, idx);
+      if (p.median) {
+        flush_hist(p, s, v);
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0)
-          s.flag = __ldcg(&p.ctl[v].npos) && (atomicAdd(&p.ctl[v].collect_done, 1u) == (unsigned)p.TC - 1);
+        if (threadIdx.x == 0) s.flag = (atomicAdd(&p.ctl[v].tiles_done, 1u) == (unsigned)p.TE - 1);
         __syncthreads();
         if (s.flag) {
           __threadfence();
-          run_select(p, s, v);
+          find_median_bins(p, s, v);
         }
-        __syncthreads();
-        continue;
       }
-      off -= p.TC;
+    } else if (kind == TASK_C) {
+      run_collect(p, s, v, idx, pol_mid);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0)
+        s.flag = __ldcg(&p.ctl[v].npos) &&
+                 (atomicAdd(&p.ctl[v].collect_done, 1u) == (unsigned)p.TC - 1);
+      __syncthreads();
+      if (s.flag) {
+        __threadfence();
+        run_select(p, s, v);
+      }
+    } else {
+      run_apply(p, s, v, idx, pol_out);
     }
-    run_apply(p, s, (int)(st - LAG2), (int)off);
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------- host side
 struct Layout {
-  size_t ctl, hist, cand, queue, total;
+  size_t ctl, hist, hist2, cand, queue, zero_bytes, total;
 };
 
 Layout layout(long long B, long long npx, bool median) {
@@ -534,27 +688,37 @@ Layout layout(long long B, long long npx, bool median) {
   off = align_up(off + sizeof(ViewCtl) * (size_t)B, 256);
   L.hist = off;
   off = align_up(off + sizeof(unsigned) * NB * (size_t)B, 256);
+  L.hist2 = off;
+  off = align_up(off + sizeof(unsigned) * 2 * NB2 * (size_t)RING, 256);
+  L.zero_bytes = off;
   L.cand = off;
   if (median) off = align_up(off + sizeof(double) * (size_t)npx * (size_t)(B < RING ? B : RING), 256);
   L.total = off;
   return L;
 }
 
-template <bool FAST>
-int blocks_per_sm() {
+typedef void (*KernelFn)(Params);
+
+template <bool FAST, int CH, bool F64>
+int blocks_for() {
   static int cached = -1;
   if (cached < 0) {
     int n = 0;
-    if (cudaFuncSetAttribute(edge_persistent_kernel<FAST>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto fn = edge_persistent_kernel<FAST, CH, F64>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(Smem)) != cudaSuccess)
       return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, edge_persistent_kernel<FAST>, NT,
-                                                      sizeof(Smem)) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, NT, sizeof(Smem)) != cudaSuccess)
       return 0;
     cached = n;
   }
   return cached;
+}
+
+template <bool FAST, int CH, bool F64>
+void pick(KernelFn& fn, int& bps) {
+  fn = edge_persistent_kernel<FAST, CH, F64>;
+  bps = blocks_for<FAST, CH, F64>();
 }
 
 int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -565,8 +729,9 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   p.queue = (unsigned long long*)(w + L.queue);
   p.ctl = (ViewCtl*)(w + L.ctl);
   p.hist = (unsigned*)(w + L.hist);
+  p.hist2 = (unsigned*)(w + L.hist2);
   p.cand = (double*)(w + L.cand);
-  IGS_CUDA_TRY(cudaMemsetAsync(w, 0, L.cand, stream));  // queue, ctl, hist
+  IGS_CUDA_TRY(cudaMemsetAsync(w, 0, L.zero_bytes, stream));  // queue, ctl, hist, hist2
   if (p.mode == MODE_FUSED) {
     p.tiles_x = (int)((p.W + TW - 1) / TW);
     p.tiles_y = (int)((p.H + TH - 1) / TH);
@@ -578,16 +743,20 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   p.TA = p.TC;
   p.total_tasks = (long long)(p.TE + p.TC + p.TA) * p.B;
   const bool fast = p.sym && !p.skip;
-  int bps = fast ? blocks_per_sm<true>() : blocks_per_sm<false>();
+  KernelFn fn = nullptr;
+  int bps = 0;
+  if (p.mode == MODE_MEDIAN_ONLY) pick<true, 1, true>(fn, bps);
+  else if (p.channels == 3 && p.in_f64) fast ? pick<true, 3, true>(fn, bps) : pick<false, 3, true>(fn, bps);
+  else if (p.channels == 3) fast ? pick<true, 3, false>(fn, bps) : pick<false, 3, false>(fn, bps);
+  else if (p.in_f64) fast ? pick<true, 1, true>(fn, bps) : pick<false, 1, true>(fn, bps);
+  else fast ? pick<true, 1, false>(fn, bps) : pick<false, 1, false>(fn, bps);
   if (bps <= 0) return IGS_ERR_CUDA;
   long long grid = (long long)bps * sm_count();
   if (grid > p.total_tasks) grid = p.total_tasks;
   if (grid < 1) grid = 1;
   void* args[] = {&p};
-  const void* fn = fast ? (const void*)edge_persistent_kernel<true>
-                        : (const void*)edge_persistent_kernel<false>;
-  IGS_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(NT), args, sizeof(Smem),
-                                           stream));
+  IGS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)grid), dim3(NT), args,
+                                           sizeof(Smem), stream));
   return IGS_OK;
 }
 

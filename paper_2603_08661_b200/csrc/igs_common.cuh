@@ -124,6 +124,63 @@ __device__ __forceinline__ double hypot_glibc(double x, double y) {
   return hypot_kernel(ax, ay);
 }
 
+// Reciprocal to ~full double precision (NOT correctly rounded): MUFU seed + two Newton steps.
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+// hypot_kernel with the correction quotient (t1+t2)/(2h) from rcp_nr instead of an IEEE
+// division.  The correction is below one ulp of h, so a relative error of ~2^-52 in it can
+// change fl(h - q) only when h - q lies within ~2^-51 ulp(h) of a rounding boundary.  The
+// sqrt and t1, t2 keep glibc's exact operation order.
+__device__ __forceinline__ double hypot_kernel_fast(double ax, double ay) {
+  double h = sqrt(ax * ax + ay * ay);
+  double t1, t2;
+  if (h <= ay + ay) {
+    double d = h - ay;
+    t1 = ((d + d) - ax) * ax;
+    double two_diff = (ax - ay) + (ax - ay);
+    t2 = (d - two_diff) * d;
+  } else {
+    double d = h - ax;
+    t1 = (d + d) * (ax - (ay + ay));
+    t2 = ((4.0 * d) - ay) * ay + d * d;
+  }
+  return h - (t1 + t2) * rcp_nr(h + h);
+}
+
+__device__ __forceinline__ double hypot_glibc_fast(double x, double y) {
+  double ax = fabs(x), ay = fabs(y);
+  if (ax < ay) {
+    double t = ax;
+    ax = ay;
+    ay = t;
+  }
+  // common case first: 2^-459 <= ay, ax <= 2^511 and ay > ax * 2^-54
+  if (ay >= 0x1p-459 && ax <= 0x1p+511 && ay > ax * 0x1p-54) return hypot_kernel_fast(ax, ay);
+  return hypot_glibc(x, y);
+}
+
+// np.clip(x, 0, 1) on the bit pattern (integer pipe): NaN kept, x <= 0 (incl. -0) -> +0.
+__device__ __forceinline__ double np_clip01_int(double x) {
+  long long b = __double_as_longlong(x);
+  if ((b & 0x7fffffffffffffffLL) > 0x7ff0000000000000LL) return x;  // NaN
+  if (b <= 0) return 0.0;                                             // +0, -0, negatives
+  return b > 0x3ff0000000000000LL ? 1.0 : x;
+}
+
+// Correctly rounded x / d given rd = RN(1/d) (Markstein: one FMA-residual correction).
+__device__ __forceinline__ double div_by(double x, double d, double rd) {
+  double q = x * rd;
+  double r = fma(-q, d, x);
+  return fma(r, rd, q);
+}
+
 // NMS direction bin of the gradient (gx, gy) -- identical to
 // np_orientation_bin(np_mod(atan2(gy, gx), pi)) except within ~1e-12 rad of a
 // bin boundary, where it falls back to evaluating that expression.

@@ -202,10 +202,33 @@ def _blur_sigma_check(sigma):
 
 
 def importance_batch(images, sigma: float = 1.0, *, out=None, nms: bool = True,
-                     median: bool = True):
+                     median: bool = True, chunk: int = 8):
     """Batched importance maps with per-view medians: (B, H, W, 3) RGB or (B, H, W) gray,
-    float32 or float64 -> (B, H, W) float64.  Equal to stacking importance_pipeline(view)."""
+    float32 or float64 -> (B, H, W) float64.  Equal to stacking importance_pipeline(view).
+
+    CUDA input: one fused launch over the whole batch, result on the device.
+    Host input (numpy array or CPU tensor; pin it for full PCIe bandwidth): streamed through
+    the GPU in chunks of ``chunk`` views with the host->device copy of chunk i+1, the fused
+    kernel on chunk i and the device->host copy of chunk i-1 overlapped on three streams;
+    the result comes back on the host (numpy for numpy input, else a CPU tensor / ``out``).
+    """
+    _blur_sigma_check(sigma)
+    on_host = not (isinstance(images, torch.Tensor) and images.is_cuda)
+    if on_host:
+        return _importance_batch_host(images, sigma, out, nms, median, chunk)
     img, np_out = _as_cuda(images, (torch.float32, torch.float64))
+    channels, (b, h, w) = _batch_geometry(img)
+    if out is None:
+        out = torch.empty((b, h, w), dtype=torch.float64, device=img.device)
+    elif tuple(out.shape) != (b, h, w) or out.dtype != torch.float64 or not out.is_cuda:
+        raise ValueError("out must be a CUDA float64 tensor of shape (B, H, W)")
+    flags = (0 if nms else _lib.IGS_EDGE_NO_NMS) | (0 if median else _lib.IGS_EDGE_NO_MEDIAN)
+    if b:
+        _edge_launch(img, channels, b, h, w, sigma, flags, out)
+    return _ret(out, np_out)
+
+
+def _batch_geometry(img):
     if img.ndim == 4:
         if img.shape[3] != 3:
             raise ValueError("expected (B, H, W, 3) RGB views or (B, H, W) gray views")
@@ -217,12 +240,77 @@ def importance_batch(images, sigma: float = 1.0, *, out=None, nms: bool = True,
     b, h, w = img.shape[:3]
     if h < 3 or w < 3:
         raise ValueError("Sobel gradients need a grayscale image of at least 3x3")
-    _blur_sigma_check(sigma)
+    return channels, (b, h, w)
+
+
+_STREAMS: dict = {}
+
+
+def _pipeline_streams(dev):
+    key = dev.index
+    if key not in _STREAMS:
+        _STREAMS[key] = tuple(torch.cuda.Stream(dev) for _ in range(3))
+    return _STREAMS[key]
+
+
+def _importance_batch_host(images, sigma, out, nms, median, chunk):
+    np_in = not isinstance(images, torch.Tensor)
+    if np_in:
+        a = np.asarray(images)
+        if a.dtype not in (np.float32, np.float64):
+            a = a.astype(np.float64)
+        src = torch.from_numpy(np.ascontiguousarray(a))
+    else:
+        src = images.contiguous()
+        if src.dtype not in (torch.float32, torch.float64):
+            src = src.to(torch.float64)
+    channels, (b, h, w) = _batch_geometry(src)
     if out is None:
-        out = torch.empty((b, h, w), dtype=torch.float64, device=img.device)
-    elif tuple(out.shape) != (b, h, w) or out.dtype != torch.float64 or not out.is_cuda:
-        raise ValueError("out must be a CUDA float64 tensor of shape (B, H, W)")
+        res = torch.empty((b, h, w), dtype=torch.float64, pin_memory=src.is_pinned())
+    else:
+        res = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
+        if tuple(res.shape) != (b, h, w) or res.dtype != torch.float64 or res.is_cuda:
+            raise ValueError("out must be a host float64 array of shape (B, H, W)")
+    dev = _device()
     flags = (0 if nms else _lib.IGS_EDGE_NO_NMS) | (0 if median else _lib.IGS_EDGE_NO_MEDIAN)
-    if b:
-        _edge_launch(img, channels, b, h, w, sigma, flags, out)
-    return _ret(out, np_out)
+    chunk = max(1, min(int(chunk), b)) if b else 1
+    nbuf = 2
+    d_in = [torch.empty((chunk,) + tuple(src.shape[1:]), dtype=src.dtype, device=dev)
+            for _ in range(nbuf)]
+    d_out = [torch.empty((chunk, h, w), dtype=torch.float64, device=dev) for _ in range(nbuf)]
+    s_h2d, s_cmp, s_d2h = _pipeline_streams(dev)
+    cur = torch.cuda.current_stream(dev)
+    for s in (s_h2d, s_cmp, s_d2h):
+        s.wait_stream(cur)
+    ev_in_free = [None] * nbuf    # compute finished reading d_in[k]
+    ev_out_free = [None] * nbuf   # D2H finished reading d_out[k]
+    for i, v0 in enumerate(range(0, b, chunk)):
+        k, n = i % nbuf, min(chunk, b - v0)
+        with torch.cuda.stream(s_h2d):
+            if ev_in_free[k] is not None:
+                s_h2d.wait_event(ev_in_free[k])
+            d_in[k][:n].copy_(src[v0:v0 + n], non_blocking=True)
+            ev_loaded = torch.cuda.Event()
+            ev_loaded.record(s_h2d)
+        with torch.cuda.stream(s_cmp):
+            s_cmp.wait_event(ev_loaded)
+            if ev_out_free[k] is not None:
+                s_cmp.wait_event(ev_out_free[k])
+            _edge_launch(d_in[k], channels, n, h, w, sigma, flags, d_out[k])
+            ev_done = torch.cuda.Event()
+            ev_done.record(s_cmp)
+            ev_in_free[k] = ev_done
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(ev_done)
+            res[v0:v0 + n].copy_(d_out[k][:n], non_blocking=True)
+            ev_o = torch.cuda.Event()
+            ev_o.record(s_d2h)
+            ev_out_free[k] = ev_o
+    for s in (s_h2d, s_cmp, s_d2h):
+        cur.wait_stream(s)
+    for t in d_in + d_out:
+        t.record_stream(cur)
+    torch.cuda.current_stream(dev).synchronize()
+    if np_in and out is None:
+        return res.numpy()
+    return out if out is not None else res
