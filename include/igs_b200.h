@@ -53,6 +53,11 @@ const char* igs_strerror(int status);
 const char* igs_last_cuda_error(void);
 int igs_abi_version(void);
 
+/* L2 set-aside for persisting (evict_last) lines: the fused edge kernel keeps the in-flight
+ * views' thinned maps evict_last.  Device-wide (cudaLimitPersistingL2CacheSize), clamped to
+ * the device maximum; *granted (nullable) receives the size in effect. */
+int igs_l2_set_aside(size_t bytes, size_t* granted);
+
 /* ---- edge-importance map (edge_pipeline.py) ----------------------------- */
 
 /* Workspace for igs_edge_importance / igs_median_normalize over `batch` views of height x width. */
@@ -84,6 +89,11 @@ int igs_nms_thin(const double* magnitude, const double* orientation, int64_t bat
 int igs_median_normalize(const double* in, int64_t batch, int64_t n, double* out,
                          double* medians, void* workspace, size_t workspace_bytes,
                          void* stream);
+
+/* Debug: record {start_ns, end_ns, kind, view, index, smid} (32 bytes) per task of later
+ * igs_edge_importance launches into the device buffer buf (NULL disables); *written (nullable)
+ * receives the number of records the previous launches produced. */
+int igs_debug_edge_trace(void* buf, int64_t capacity, int64_t* written);
 
 /* ---- budgeted candidate selection (densify_controller.py:66-106) -------- */
 

@@ -29,6 +29,7 @@ SIGNATURES = {
     "igs_strerror": (C.c_char_p, [_int]),
     "igs_last_cuda_error": (C.c_char_p, []),
     "igs_abi_version": (_int, []),
+    "igs_l2_set_aside": (_int, [_sz, _szp]),
     "igs_edge_workspace_bytes": (_int, [_i64, _i64, _i64, _int, _szp]),
     "igs_edge_importance": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _int, _vp, _vp, _sz,
                                    _vp]),
@@ -37,6 +38,7 @@ SIGNATURES = {
     "igs_sobel_gradients": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "igs_nms_thin": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "igs_median_normalize": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "igs_debug_edge_trace": (_int, [_vp, _i64, C.POINTER(C.c_int64)]),
     "igs_select_workspace_bytes": (_int, [_i64, _szp]),
     "igs_select_candidates": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _i64, _vp, _vp, _vp,
                                      _sz, _vp]),

@@ -43,4 +43,17 @@ const char* igs_last_cuda_error(void) { return igs::g_cuda_error; }
 
 int igs_abi_version(void) { return 1; }
 
+// L2 set-aside for persisting (evict_last) lines on the current device; returns the granted
+// size in *granted (nullable).  Device-wide setting (cudaLimitPersistingL2CacheSize).
+int igs_l2_set_aside(size_t bytes, size_t* granted) {
+  int dev = 0;
+  IGS_CUDA_TRY(cudaGetDevice(&dev));
+  int maxp = 0;
+  IGS_CUDA_TRY(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  if (bytes > (size_t)maxp) bytes = (size_t)maxp;
+  IGS_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+  if (granted) IGS_CUDA_TRY(cudaDeviceGetLimit(granted, cudaLimitPersistingL2CacheSize));
+  return IGS_OK;
+}
+
 }  // extern "C"

@@ -3,22 +3,23 @@
 // Replaces splitkit.edge_pipeline.importance_pipeline and its stages
 // (/root/reference/pkg/src/splitkit/edge_pipeline.py:42-135).
 //
-// Task kinds, handed out in queue order by an atomic counter (every task
-// depends only on tasks handed out earlier, and the grid is co-resident, so
-// spinning on a dependency always terminates):
+// Task kinds (one persistent cooperative grid, 256-thread blocks):
 //   E(v,t)  fused tile: gray -> 5x5 blur -> Sobel -> |g| + direction bin -> NMS
 //           for a TH x TW output tile staged in shared memory with a 4-pixel
 //           halo; writes the thinned map and merges a per-view histogram of the
 //           positive survivors.  The last E task of a view locates the median
 //           histogram bin(s).                                 (:42-114, :123)
 //   C(v,c)  collect: gathers the values falling in the median bin(s) into a
-//           candidate buffer.  The last C task radix-selects the exact order
-//           statistic(s) -> median m (np.median: (a+b)/2 for an even count). (:124)
-//   A(v,c)  apply: out = min(v / (2 m), 1) in place.                   (:125)
-// Queue order per step s: E(s) tiles, C(s-LAG1) chunks, A(s-LAG2) chunks, so
-// at most LAG2+1 views' thinned maps are live; they are stored with an L2
-// evict_last policy (the input streams with evict_first), so E, C and A meet in
-// L2 and the final map is written back to HBM once.
+//           candidate buffer plus a level-2 histogram.  The last C task of a view
+//           selects the exact order statistic(s) -> median m (np.median: (a+b)/2
+//           for an even count).                                          (:124)
+//   A(v,c)  apply: out = min(v / (2 m), 1) in place.                     (:125)
+// Scheduling is dependency driven (claim_task): A work of views whose median is
+// published first, then C work of views whose bins are published, else the next
+// E tile -- at most AHEAD views past the A front, so only a few views' thinned
+// maps are live.  Those are stored with an L2 evict_last policy (the input
+// streams with evict_first), so E, C and A meet in L2 and the final map is
+// written back to HBM once.  Work is claimed only when ready: no task waits.
 //
 // Arithmetic: float64 in scipy's order (see oracle/edge.py): taps summed in
 // row-major order from 0.0 with separately rounded multiply and add; glibc's
@@ -48,12 +49,16 @@ static_assert(BW * (BH / SB) == NT && BH % SB == 0, "blur strips must cover the 
 static_assert(MH * MW <= GH * GW, "magnitude aliases the gray buffer");
 static_assert(GW <= 96, "phase A covers a row with three lanes per warp lane");
 
-constexpr int NB = 2048;                     // level-1 median histogram: 16 bins per octave
-constexpr int HIST_BASE = 14768;             // (bits>>48) of 2^-100; bins cover [2^-100, 2^28)
+constexpr int NB = 4096;                     // level-1 median histogram: 64 bins per octave
+constexpr int HIST_SHIFT = 46;               // bin = (bits >> 46) - HIST_BASE (18 top bits)
+constexpr int HIST_BASE = 963 << 6;          // bins cover [2^-60, 2^4); outside -> end bins
+constexpr int NBR = 2048;                    // radix-select digit bins (11 bits)
+constexpr int SUB_SHIFT = 34;                // level-2 bin = bits 45..34 inside a level-1 bin
+constexpr int SLOTS = 8;                     // candidates kept per level-2 bin
 constexpr int NB2 = 4096;                    // level-2 histogram: bits 47..36 inside a bin
-constexpr int CHUNK = 32768;                 // pixels per collect/apply task
-constexpr int LAG1 = 2, LAG2 = 4;            // queue lags of C and A behind E
-constexpr int RING = LAG2 + 3;               // candidate buffers / level-2 histograms in flight
+constexpr int CHUNK = 16384;                 // pixels per collect/apply task (< 65536)
+constexpr int AHEAD = 5;                     // E may run at most AHEAD views past the A front
+constexpr int RING = AHEAD + 2;              // candidate buffers / level-2 histograms in flight
 constexpr int SEL_CAP = (GH * GW + BH * BW); // doubles of smem the select may use
 
 enum Mode { MODE_FUSED = 0, MODE_MEDIAN_ONLY = 1 };
@@ -69,7 +74,8 @@ struct ViewCtl {            // per-view control block, zeroed before launch
   unsigned long long npos;  // positive count
   double denom;             // 2 * median
   double median;
-  unsigned pad[14];
+  unsigned c_claim, a_claim;// C / A chunks handed out
+  unsigned pad[12];
 };
 static_assert(sizeof(ViewCtl) == 128, "one ViewCtl per 128-byte line");
 
@@ -91,12 +97,12 @@ struct Params {
   double* medians;          // optional (B,) output of the medians
   // scheduling
   int tiles_x, tiles_y, TE, TC, TA;
-  long long total_tasks;
   // workspace
-  unsigned long long* queue;
+  unsigned* sched;          // [1] C front view, [2] A front view, [4..5] next E task (u64)
   ViewCtl* ctl;
   unsigned* hist;           // (B, NB)
   unsigned* hist2;          // (RING, 2, NB2)
+  double* slots;            // (RING, 2, NB2, SLOTS) candidates bucketed by level-2 bin
   double* cand;             // (RING, npx)
 };
 
@@ -104,10 +110,12 @@ struct __align__(16) Smem {
   double g[GH * GW];        // gray, then gradient magnitude; select scratch
   double b[BH * BW];        // blurred; select scratch (contiguous with g)
   uint8_t bin[TH * TW];     // NMS direction bins of the output tile
-  unsigned hist[NB];
+  unsigned hist[NB / 2];    // level-1 counts packed two 16-bit bins per word; radix scratch
   unsigned warp_sums[32];
   int task_kind, task_view, task_idx, flag;
   int ivals[4];
+  int scratch[4];
+  unsigned long long mbar[2];  // bulk-copy barriers of the C / A streams
   unsigned long long u64[2];
 };
 
@@ -124,12 +132,12 @@ __device__ __forceinline__ unsigned long long policy_evict_last() {
 }
 __device__ __forceinline__ double ld_hint(const double* a, unsigned long long pol) {
   double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
   return v;
 }
 __device__ __forceinline__ double ld_hint(const float* a, unsigned long long pol) {
   float v;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
   return (double)v;
 }
 __device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
@@ -141,14 +149,50 @@ __device__ __forceinline__ double ld_cg_hint(const double* a, unsigned long long
   return v;
 }
 
+// ---- TMA bulk copies (cp.async.bulk global -> shared, completion on an mbarrier) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ int clamp_i(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 __device__ __forceinline__ long long clampi(long long v, long long lo, long long hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }
 
+__device__ __forceinline__ int y0_row(int ty, int r, int H) { return clamp_i(ty * TH - 4 + r, 0, H - 1); }
+
 __device__ __forceinline__ int hist_bin(double v) {
-  long long hb = (long long)((unsigned long long)__double_as_longlong(v) >> 48) - HIST_BASE;
+  long long hb = (long long)((unsigned long long)__double_as_longlong(v) >> HIST_SHIFT) - HIST_BASE;
   return hb < 0 ? 0 : (hb >= NB ? NB - 1 : (int)hb);
+}
+
+// Shared-memory level-1 histogram: two 16-bit counters per word (a task adds < 65536).
+__device__ __forceinline__ void hist_add(Smem& s, int b) {
+  atomicAdd(&s.hist[b >> 1], 1u << ((b & 1) << 4));
 }
 
 // ---------------------------------------------------------------- E: fused tile
@@ -187,6 +231,9 @@ __device__ __forceinline__ void phase_gray(const Params& p, Smem& s, int v, int 
     }
   }
 }
+
+template <int CH, bool F64>
+__device__ void claim_next(const Params& p, Smem& s, unsigned long long pol_in);
 
 template <bool FAST, int CH, bool F64>
 __device__ void run_tile(const Params& p, Smem& s, int v, int t, unsigned long long pol_in,
@@ -231,7 +278,12 @@ __device__ void run_tile(const Params& p, Smem& s, int v, int t, unsigned long l
       }
     }
 #pragma unroll
-    for (int o = 0; o < SB; ++o) s.b[(u0 + o) * BW + c] = np_clip01_int(acc[o]);
+    for (int o = 0; o < SB; ++o) {
+      // RGB input: gray in [0, 1] and positive weights keep the sum >= +0, so only the
+      // upper clip can bite (NaN passes through as in np.clip).  Gray input: full clip.
+      const double x = acc[o];
+      s.b[(u0 + o) * BW + c] = (CH == 3) ? (x > 1.0 ? 1.0 : x) : np_clip01_int(x);
+    }
   }
   __syncthreads();
   // Border tiles: out-of-image blurred cells take the value of the clamped in-image cell.
@@ -256,54 +308,79 @@ __device__ void run_tile(const Params& p, Smem& s, int v, int t, unsigned long l
   }
 
   // Phase C: Sobel (NI_Correlate tap order; the zero taps are skipped as scipy does; the
-  // exact x2 taps as FMAs), glibc hypot, direction bin of the output pixels.
-  for (int i = tid; i < MH * MW; i += NT) {
-    const int u = i / MW, c = i - u * MW;
-    const int y = y0 - 1 + u, x = x0 - 1 + c;
-    double m = 0.0;  // out-of-image neighbours count as 0 for NMS (edge_pipeline.py:97)
-    if (y >= 0 && y < H && x >= 0 && x < W) {
-      const double* b = &s.b[u * BW + c];
-      const double b00 = b[0], b01 = b[1], b02 = b[2];
-      const double b10 = b[BW], b12 = b[BW + 2];
-      const double b20 = b[2 * BW], b21 = b[2 * BW + 1], b22 = b[2 * BW + 2];
-      double gx = b02 - b00;              // (0 + -b00) + b02
-      gx = fma(-2.0, b10, gx);
-      gx = fma(2.0, b12, gx);
-      gx = gx - b20;
-      gx = gx + b22;
-      double gy = fma(-2.0, b01, -b00);   // (0 + -b00) + -2 b01
-      gy = gy - b02;
-      gy = gy + b20;
-      gy = fma(2.0, b21, gy);
-      gy = gy + b22;
-      m = hypot_glibc_fast(gx, gy);
-      if (p.nms && u >= 1 && u <= TH && c >= 1 && c <= TW)
-        s.bin[(u - 1) * TW + (c - 1)] = (uint8_t)gradient_bin(gx, gy);
+  // exact x2 taps as FMAs), glibc hypot, direction bin of the output pixels.  Thread (c, k)
+  // owns column c, rows 9k..9k+8 of the magnitude region and slides a 3x3 window down.
+  {
+    constexpr int SS = 9, NSTRIP = (MH + SS - 1) / SS;
+    static_assert(MW * NSTRIP <= NT, "one strip per thread");
+    const int c = tid % MW, k = tid / MW;
+    if (k < NSTRIP) {
+      const int x = x0 - 1 + c;
+      const bool xin = x >= 0 && x < W;
+      const double* col = &s.b[(k * SS) * BW + c];
+      double t0 = col[0], t1 = col[1], t2 = col[2];
+      double m0 = col[BW], m2 = col[BW + 2], m1 = col[BW + 1];
+#pragma unroll
+      for (int j = 0; j < SS; ++j) {
+        const int u = k * SS + j;
+        if (u >= MH) break;
+        const double* nb = col + (j + 2) * BW;
+        const double d0 = nb[0], d1 = nb[1], d2 = nb[2];
+        const int y = y0 - 1 + u;
+        double m = 0.0;  // out-of-image neighbours count as 0 for NMS (edge_pipeline.py:97)
+        if (xin && y >= 0 && y < H) {
+          double gx = t2 - t0;                // (0 + -b00) + b02
+          gx = fma(-2.0, m0, gx);
+          gx = fma(2.0, m2, gx);
+          gx = gx - d0;
+          gx = gx + d2;
+          double gy = fma(-2.0, t1, -t0);     // (0 + -b00) + -2 b01
+          gy = gy - t2;
+          gy = gy + d0;
+          gy = fma(2.0, d1, gy);
+          gy = gy + d2;
+          m = (CH == 3) ? hypot_glibc_fast_bounded(gx, gy) : hypot_glibc_fast(gx, gy);
+          if (p.nms && u >= 1 && u <= TH && c >= 1 && c <= TW)
+            s.bin[(u - 1) * TW + (c - 1)] = (uint8_t)gradient_bin(gx, gy);
+        }
+        s.g[u * MW + c] = m;  // gray is dead after phase B
+        t0 = m0; t1 = m1; t2 = m2;
+        m0 = d0; m1 = d1; m2 = d2;
+      }
     }
-    s.g[i] = m;  // gray is dead after phase B
   }
   __syncthreads();
 
   // Phase D: NMS (keep iff m > prev and m >= next; magnitudes are >= +0 or NaN, so the
   // comparisons run on the bit patterns), store with L2 evict_last, histogram survivors.
-  for (int i = tid; i < TH * TW; i += NT) {
-    const int a = i / TW, c = i - a * TW;
-    const int y = y0 + a, x = x0 + c;
-    if (y >= H || x >= W) continue;
-    const double* mp = &s.g[(a + 1) * MW + (c + 1)];
-    const double m = *mp;
-    double outv = m;
-    if (p.nms) {
-      const int bn = s.bin[i];
-      const int po = bn == 0 ? -1 : (bn == 1 ? -MW - 1 : (bn == 2 ? -MW : -MW + 1));
-      const long long mb = __double_as_longlong(m);
-      const bool keep = (mb <= 0x7ff0000000000000LL) &&
-                        (mb > __double_as_longlong(mp[po])) &&
-                        (mb >= __double_as_longlong(mp[-po]));
-      outv = keep ? m : 0.0;
+  if (tid == 0) claim_next<CH, F64>(p, s, pol_in);
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int a = warp; a < TH; a += NWARP) {
+      const int y = y0 + a;
+      if (y >= H) break;
+      double* orow = p.out + vbase + (long long)y * W + x0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int c = lane + 32 * k;
+        if (c >= TW || x0 + c >= W) continue;
+        const double* mp = &s.g[(a + 1) * MW + (c + 1)];
+        const double m = *mp;
+        double outv = m;
+        if (p.nms) {
+          const int bn = s.bin[a * TW + c];
+          const int po = bn == 0 ? -1 : (bn == 1 ? -MW - 1 : (bn == 2 ? -MW : -MW + 1));
+          const long long mb = __double_as_longlong(m);
+          const bool keep = (mb <= 0x7ff0000000000000LL) &&
+                            (mb > __double_as_longlong(mp[po])) &&
+                            (mb >= __double_as_longlong(mp[-po]));
+          outv = keep ? m : 0.0;
+        }
+        st_hint(orow + c, outv, pol_mid);
+        if (p.median && outv > 0.0) hist_add(s, hist_bin(outv));
+      }
     }
-    st_hint(p.out + vbase + (long long)y * W + x, outv, pol_mid);
-    if (p.median && outv > 0.0) atomicAdd(&s.hist[hist_bin(outv)], 1u);
   }
 }
 
@@ -313,7 +390,7 @@ __device__ void run_hist_chunk(const Params& p, Smem& s, int v, int c) {
   const double* src = (const double*)p.img + (long long)v * p.npx;
   for (long long i = lo + threadIdx.x; i < hi; i += NT) {
     double x = __ldg(src + i);
-    if (x > 0.0) atomicAdd(&s.hist[hist_bin(x)], 1u);
+    if (x > 0.0) hist_add(s, hist_bin(x));
   }
 }
 
@@ -321,10 +398,11 @@ __device__ void run_hist_chunk(const Params& p, Smem& s, int v, int c) {
 __device__ void flush_hist(const Params& p, Smem& s, int v) {
   __syncthreads();
   unsigned* gh = p.hist + (long long)v * NB;
-  for (int i = threadIdx.x; i < NB; i += NT) {
-    unsigned h = s.hist[i];
+  for (int i = threadIdx.x; i < NB / 2; i += NT) {
+    const unsigned h = s.hist[i];
     if (h) {
-      atomicAdd(&gh[i], h);
+      if (h & 0xffffu) atomicAdd(&gh[2 * i], h & 0xffffu);
+      if (h >> 16) atomicAdd(&gh[2 * i + 1], h >> 16);
       s.hist[i] = 0;
     }
   }
@@ -394,65 +472,134 @@ __device__ void find_median_bins(const Params& p, Smem& s, int v) {
       ctl.r2 = r2;
     }
   }
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     if (total == 0) atomicExch(&ctl.select_done, 1u);
     atomicExch(&ctl.binfound, 1u);
   }
 }
 
-__device__ __forceinline__ int sub_bin(unsigned long long bits) { return (int)((bits >> 36) & (NB2 - 1)); }
+__device__ __forceinline__ int sub_bin(unsigned long long bits) {
+  return (int)((bits >> SUB_SHIFT) & (NB2 - 1));
+}
+
+// ---------------------------------------------------- streamed chunks for C and A tasks
+// A C/A task streams its chunk of the thinned map through shared memory in PIECE-sized
+// pieces with TMA bulk copies (two buffers in flight, mbarrier completion), so the task is
+// not limited by register-held loads.  Unaligned views fall back to plain loads.
+constexpr int PIECE = 2048;                     // doubles per piece (16 KB)
+constexpr int STAGE = 256;                      // staged candidates per list in a C task
+static_assert(2 * PIECE + 2 * STAGE <= GH * GW + BH * BW, "stream buffers fit in g + b");
+
+// g and b are contiguous doubles at the start of Smem: one arena for C/A/select scratch.
+__device__ __forceinline__ double* arena(Smem& s) { return reinterpret_cast<double*>(&s); }
+
+template <typename Visit>
+__device__ void stream_chunk(Smem& s, const double* src, long long lo, long long hi,
+                             Visit visit) {
+  double* buf0 = arena(s);
+  double* buf1 = arena(s) + PIECE;
+  const long long n = hi - lo;
+  const bool aligned = ((((uintptr_t)(src + lo)) & 15) == 0);
+  if (!aligned) {
+    for (long long i = lo + threadIdx.x; i < hi; i += NT) visit(i, __ldcg(src + i));
+    return;
+  }
+  const long long nfull = n & ~1ll;  // bulk part: a multiple of 16 bytes
+  const int npieces = (int)((nfull + PIECE - 1) / PIECE);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_init(&s.mbar[0]);
+    mbar_init(&s.mbar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async();
+    for (int k = 0; k < 2 && k < npieces; ++k) {
+      const long long off = (long long)k * PIECE;
+      const unsigned len = (unsigned)min((long long)PIECE, nfull - off);
+      bulk_load(k ? buf1 : buf0, src + lo + off, len * 8u, &s.mbar[k]);
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < npieces; ++k) {
+    double* buf = (k & 1) ? buf1 : buf0;
+    mbar_wait(&s.mbar[k & 1], (unsigned)((k >> 1) & 1));
+    const long long off = (long long)k * PIECE;
+    const int len = (int)min((long long)PIECE, nfull - off);
+    for (int i = threadIdx.x; i < len; i += NT) visit(lo + off + i, buf[i]);
+    __syncthreads();
+    if (threadIdx.x == 0 && k + 2 < npieces) {
+      fence_proxy_async();
+      const long long o2 = (long long)(k + 2) * PIECE;
+      const unsigned l2 = (unsigned)min((long long)PIECE, nfull - o2);
+      bulk_load(buf, src + lo + o2, l2 * 8u, &s.mbar[k & 1]);
+    }
+  }
+  if ((n & 1) && threadIdx.x == 0) visit(hi - 1, __ldcg(src + hi - 1));
+  __syncthreads();
+}
 
 // ------------------------------------------------------------- C: collect candidates
-__device__ void append(double x, bool f, unsigned* counter, double* base, int dir,
-                       unsigned* h2) {
-  const unsigned m = __ballot_sync(0xffffffffu, f);
-  if (!m) return;
-  unsigned slot = 0;
-  const int leader = __ffs(m) - 1;
-  if ((int)lane_id() == leader) slot = atomicAdd(counter, __popc(m));
-  slot = __shfl_sync(0xffffffffu, slot, leader);
-  if (f) {
-    base[dir * (long long)(slot + __popc(m & lanemask_lt()))] = x;
-    atomicAdd(&h2[sub_bin((unsigned long long)__double_as_longlong(x))], 1u);
+// Candidates are bucketed by level-2 bin (returning atomics on the level-2 histogram) and
+// also appended to a flat per-view list: staged in shared memory, then ONE global atomic per
+// task reserves the space.
+__device__ __forceinline__ void stage(Smem& s, double x, int list, double* overflow_base,
+                                      int dir, unsigned* gcounter) {
+  double* buf = arena(s) + 2 * PIECE + list * STAGE;
+  const int k = atomicAdd(&s.ivals[1 + list], 1);
+  if (k < STAGE) {
+    buf[k] = x;
+  } else {  // rare: more than STAGE candidates in one chunk
+    const unsigned g = atomicAdd(gcounter, 1u);
+    overflow_base[dir * (long long)g] = x;
   }
 }
 
-__device__ void run_collect(const Params& p, Smem& s, int v, int c, unsigned long long pol_mid) {
+__device__ void run_collect(const Params& p, Smem& s, int v, int c) {
   ViewCtl& ctl = p.ctl[v];
-  if (threadIdx.x == 0) {
-    spin_until_geq(&ctl.binfound, 1u);
-    if (v >= RING) spin_until_geq(&p.ctl[v - RING].select_done, 1u);  // ring slot free
+  if (threadIdx.x == 0) {  // claimed only once binfound (and the ring slot) is published
     s.ivals[0] = __ldcg(&ctl.npos) ? 1 : 0;
-    s.ivals[1] = __ldcg(&ctl.b1);
-    s.ivals[2] = __ldcg(&ctl.b2);
+    s.ivals[1] = 0;
+    s.ivals[2] = 0;
+    s.scratch[0] = __ldcg(&ctl.b1);
+    s.scratch[1] = __ldcg(&ctl.b2);
   }
   __syncthreads();
-  if (!s.ivals[0]) return;
-  const int b1 = s.ivals[1], b2 = s.ivals[2];
+  const int npos = s.ivals[0], b1 = s.scratch[0], b2 = s.scratch[1];
+  __syncthreads();
+  if (!npos) return;
   const double* src = (p.mode == MODE_FUSED) ? p.out + (long long)v * p.npx
                                              : (const double*)p.img + (long long)v * p.npx;
   const int slot = v % RING;
   double* cand = p.cand + (long long)slot * p.npx;
+  double* cand2 = cand + p.npx - 1;
   unsigned* h2a = p.hist2 + (long long)slot * 2 * NB2;
   unsigned* h2b = h2a + NB2;
+  double* sla = p.slots + (long long)slot * 2 * NB2 * SLOTS;
+  double* slb = sla + NB2 * SLOTS;
   const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
-  constexpr int U = 8;
-  for (long long base = lo; base < hi; base += NT * U) {
-    double x[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const long long i = base + k * NT + threadIdx.x;
-      x[k] = i < hi ? ld_cg_hint(src + i, pol_mid) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int hb = x[k] > 0.0 ? hist_bin(x[k]) : -1;
-      append(x[k], hb == b1, &ctl.cnt1, cand, 1, h2a);
-      if (b2 != b1) append(x[k], hb == b2, &ctl.cnt2, cand + p.npx - 1, -1, h2b);
-    }
+  stream_chunk(s, src, lo, hi, [&](long long, double x) {
+    if (!(x > 0.0)) return;
+    const int hb = hist_bin(x);
+    if (hb != b1 && hb != b2) return;
+    const int list = hb == b1 ? 0 : 1;
+    const int sb = sub_bin((unsigned long long)__double_as_longlong(x));
+    const unsigned k = atomicAdd(&(list ? h2b : h2a)[sb], 1u);
+    if (k < (unsigned)SLOTS) (list ? slb : sla)[sb * SLOTS + k] = x;
+    if (list == 0) stage(s, x, 0, cand, 1, &ctl.cnt1);
+    else stage(s, x, 1, cand2, -1, &ctl.cnt2);
+  });
+  // append the staged lists: one reservation per list
+  const int n1 = min(s.ivals[1], STAGE), n2s = min(s.ivals[2], STAGE);
+  if (threadIdx.x == 0) {
+    s.u64[0] = n1 ? atomicAdd(&ctl.cnt1, (unsigned)n1) : 0u;
+    s.u64[1] = n2s ? atomicAdd(&ctl.cnt2, (unsigned)n2s) : 0u;
   }
+  __syncthreads();
+  const unsigned long long o1 = s.u64[0], o2 = s.u64[1];
+  const double* st = arena(s) + 2 * PIECE;
+  for (int k = threadIdx.x; k < n1; k += NT) cand[o1 + k] = st[k];
+  for (int k = threadIdx.x; k < n2s; k += NT) cand2[-(long long)(o2 + k)] = st[STAGE + k];
 }
 
 // Block-wide radix select over n positive doubles (bit order == value order) stored at
@@ -469,7 +616,7 @@ __device__ unsigned long long block_radix_select(Smem& s, const double* src, lon
     const int width = hb + 1 < 11 ? hb + 1 : 11;
     const int shift = hb + 1 - width;
     const unsigned dmask = (1u << width) - 1;
-    for (int i = threadIdx.x; i < NB; i += NT) h[i] = 0;
+    for (int i = threadIdx.x; i < NBR; i += NT) h[i] = 0;
     __syncthreads();
     for (long long i = threadIdx.x; i < n; i += NT) {
       const double x = global_mem ? __ldcg(src + dir * i) : src[dir * i];
@@ -479,204 +626,348 @@ __device__ unsigned long long block_radix_select(Smem& s, const double* src, lon
     __syncthreads();
     int d;
     unsigned long long r;
-    locate<NB>(h, s, rank, d, r, false);
+    locate<NBR>(h, s, rank, d, r, false);
     rank = r;
     prefix |= (unsigned long long)d << shift;
     pmask |= (unsigned long long)dmask << shift;
   }
-  for (int i = threadIdx.x; i < NB; i += NT) h[i] = 0;
+  for (int i = threadIdx.x; i < NBR; i += NT) h[i] = 0;
   __syncthreads();
   return prefix;
 }
 
-// Order statistic `rank` of the candidates of level-1 bin b (region src[dir*i], i < n) whose
-// level-2 histogram is h2: locate the level-2 bin, stage its members in shared memory and
-// radix-select the low 36 bits there.  Clamped bins (0, NB-1) and oversize level-2 bins fall
-// back to a full-width select over the whole candidate list.
-__device__ double select_in_bin(Smem& s, const double* src, long long n, int dir, int b,
-                                unsigned long long rank, const unsigned* h2) {
-  if (b == 0 || b == NB - 1)
-    return __longlong_as_double(block_radix_select(s, src, n, dir, rank, 63, true));
-  int sb;
+// Exact order statistics of the median.  For each wanted rank (one for an odd count, two for
+// an even one) the level-2 histogram of its level-1 bin names a sub-bin (bits 47..36); one
+// unrolled pass over the candidate list stages the members of the (at most two) sub-bins in
+// shared memory, where a radix select over bits 35..0 finishes.  Clamped level-1 bins
+// (0, NB-1) and oversize sub-bins fall back to a full-width select over the candidates.
+struct Want {
+  const double* src;   // candidate region, element i at src[dir * i]
+  long long n;
+  int dir;
+  int bin;             // level-1 bin
+  unsigned long long rank;
+  const unsigned* h2;
+  int sb;              // level-2 bin (-1: generic path)
   unsigned long long r2;
-  locate<NB2>(h2, s, rank, sb, r2, true);
-  const unsigned cnt = __ldcg(&h2[sb]);
-  if (cnt > (unsigned)SEL_CAP)
-    return __longlong_as_double(block_radix_select(s, src, n, dir, rank, 63, true));
-  double* buf = s.g;  // g and b are contiguous: SEL_CAP doubles
-  if (threadIdx.x == 0) s.ivals[1] = 0;
-  __syncthreads();
-  for (long long i = threadIdx.x; i < n; i += NT) {
-    const double x = __ldcg(src + dir * i);
-    if (sub_bin((unsigned long long)__double_as_longlong(x)) == sb) {
-      const int k = atomicAdd(&s.ivals[1], 1);
-      buf[k] = x;
+  unsigned cnt;
+};
+
+__device__ void gather_subbins(Smem& s, const double* src, long long n, int dir, int sbA,
+                               double* bufA, int sbB, double* bufB) {
+  constexpr int U = 8;
+  for (long long base = 0; base < n; base += NT * U) {
+    double x[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const long long i = base + k * NT + threadIdx.x;
+      x[k] = i < n ? __ldcg(src + dir * i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (base + k * NT + threadIdx.x >= n) continue;
+      const int sb = sub_bin((unsigned long long)__double_as_longlong(x[k]));
+      if (sb == sbA) bufA[atomicAdd(&s.ivals[1], 1)] = x[k];
+      else if (sb == sbB) bufB[atomicAdd(&s.ivals[2], 1)] = x[k];
     }
   }
+}
+
+// Rank selection for a short shared-memory list (n <= NT): element t's rank is the number of
+// smaller elements plus equal ones before it; the owner of rank `rank` publishes its bits.
+__device__ unsigned long long small_select(Smem& s, const double* buf, int n,
+                                           unsigned long long rank) {
+  const int t = threadIdx.x;
+  if (t < n) {
+    const unsigned long long x = (unsigned long long)__double_as_longlong(buf[t]);
+    unsigned r = 0;
+    for (int j = 0; j < n; ++j) {
+      const unsigned long long y = (unsigned long long)__double_as_longlong(buf[j]);
+      r += (y < x) || (y == x && j < t);
+    }
+    if (r == rank) s.u64[1] = x;
+  }
   __syncthreads();
-  return __longlong_as_double(block_radix_select(s, buf, cnt, 1, r2, 35, false));
+  const unsigned long long res = s.u64[1];
+  __syncthreads();
+  return res;
+}
+
+__device__ unsigned long long select_staged(Smem& s, const double* buf, unsigned n,
+                                            unsigned long long rank) {
+  if (n <= (unsigned)NT) return small_select(s, buf, (int)n, rank);
+  return block_radix_select(s, buf, n, 1, rank, 35, false);
+}
+
+__device__ void plan(Smem& s, Want& w) {
+  w.sb = -1;
+  if (w.bin == 0 || w.bin == NB - 1) return;
+  int sb;
+  unsigned long long r2;
+  locate<NB2>(w.h2, s, w.rank, sb, r2, true);
+  w.sb = sb;
+  w.r2 = r2;
+  w.cnt = __ldcg(&w.h2[sb]);
+}
+
+// Order statistic of one Want: from the bucketed slots when the level-2 bin holds at most
+// SLOTS candidates (the common case: ~1 per bin), else by staging the level-2 bin from the
+// flat candidate list, else (clamped level-1 bin) by a full-width select over the list.
+__device__ double resolve(Smem& s, const Want& w, const double* slots) {
+  if (w.sb < 0)
+    return __longlong_as_double(block_radix_select(s, w.src, w.n, w.dir, w.rank, 63, true));
+  double* buf = s.g;
+  if (w.cnt <= (unsigned)SLOTS) {
+    if (threadIdx.x < w.cnt) buf[threadIdx.x] = __ldcg(slots + w.sb * SLOTS + threadIdx.x);
+    __syncthreads();
+    return __longlong_as_double(small_select(s, buf, (int)w.cnt, w.r2));
+  }
+  if (w.cnt > (unsigned)SEL_CAP)
+    return __longlong_as_double(block_radix_select(s, w.src, w.n, w.dir, w.rank, 63, true));
+  if (threadIdx.x == 0) {
+    s.ivals[1] = 0;
+    s.ivals[2] = 0;
+  }
+  __syncthreads();
+  gather_subbins(s, w.src, w.n, w.dir, w.sb, buf, -2, buf);
+  __syncthreads();
+  return __longlong_as_double(select_staged(s, buf, w.cnt, w.r2));
 }
 
 __device__ void run_select(const Params& p, Smem& s, int v) {
   ViewCtl& ctl = p.ctl[v];
   const int slot = v % RING;
   const double* cand = p.cand + (long long)slot * p.npx;
-  unsigned* h2a = p.hist2 + (long long)slot * 2 * NB2;
-  unsigned* h2b = h2a + NB2;
+  const unsigned* h2a = p.hist2 + (long long)slot * 2 * NB2;
+  const unsigned* h2b = h2a + NB2;
+  const double* sla = p.slots + (long long)slot * 2 * NB2 * SLOTS;
+  const double* slb = sla + NB2 * SLOTS;
   const unsigned n1 = __ldcg(&ctl.cnt1), n2 = __ldcg(&ctl.cnt2);
-  const unsigned long long r1 = __ldcg(&ctl.r1), r2 = __ldcg(&ctl.r2);
   const int b1 = __ldcg(&ctl.b1), b2 = __ldcg(&ctl.b2);
   const unsigned long long npos = __ldcg(&ctl.npos);
-  const double a = select_in_bin(s, cand, n1, 1, b1, r1, h2a);
+  const bool even = (npos & 1ull) == 0;
+  Want w1{cand, n1, 1, b1, __ldcg(&ctl.r1), h2a, -1, 0, 0};
+  plan(s, w1);
+  const double a = resolve(s, w1, sla);
   double m = a;
-  if ((npos & 1ull) == 0) {
-    const double b = (b2 == b1) ? select_in_bin(s, cand, n1, 1, b1, r2, h2a)
-                                : select_in_bin(s, cand + p.npx - 1, n2, -1, b2, r2, h2b);
+  if (even) {
+    Want w2 = (b2 == b1) ? Want{cand, n1, 1, b1, __ldcg(&ctl.r2), h2a, -1, 0, 0}
+                         : Want{cand + p.npx - 1, n2, -1, b2, __ldcg(&ctl.r2), h2b, -1, 0, 0};
+    plan(s, w2);
+    const double b = resolve(s, w2, b2 == b1 ? sla : slb);
     m = (a + b) / 2.0;
   }
   // clear this slot's level-2 histograms for view v + RING
-  for (int i = threadIdx.x; i < 2 * NB2; i += NT) h2a[i] = 0;
+  unsigned* h2w = p.hist2 + (long long)slot * 2 * NB2;
+  for (int i = threadIdx.x; i < 2 * NB2; i += NT) h2w[i] = 0;
   if (threadIdx.x == 0) {
     ctl.median = m;
     ctl.denom = 2.0 * m;
     if (p.medians) p.medians[v] = m;
   }
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) atomicExch(&ctl.select_done, 1u);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(&ctl.select_done, 1u);
+  }
 }
 
 // ------------------------------------------------------------------ A: apply
+__device__ __forceinline__ double normalise(double x, double denom, double rd, bool plain) {
+  double q;
+  if (plain && x == 0.0) q = x * rd;                       // +-0 / denom, sign kept
+  else if (plain && fabs(x) < 0x1p+900 && fabs(x) > 0x1p-900) q = div_by(x, denom, rd);
+  else q = x / denom;
+  return np_min1(q);
+}
+
 __device__ void run_apply(const Params& p, Smem& s, int v, int c, unsigned long long pol_out) {
-  ViewCtl& ctl = p.ctl[v];
-  if (threadIdx.x == 0) spin_until_geq(&ctl.select_done, 1u);
-  __syncthreads();
+  ViewCtl& ctl = p.ctl[v];  // claimed only once select_done is published
   const double denom = __ldcg(&ctl.denom);
   const double rd = __drcp_rn(denom);
+  const bool plain = isfinite(denom) && denom > 0x1p-1000 && denom < 0x1p+1000;
   const double* src = (p.mode == MODE_FUSED) ? p.out + (long long)v * p.npx
                                              : (const double*)p.img + (long long)v * p.npx;
   double* dst = p.out + (long long)v * p.npx;
   const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
-  constexpr int U = 8;
-  const bool plain = isfinite(denom) && denom > 0x1p-1000 && denom < 0x1p+1000;
-  for (long long base = lo; base < hi; base += NT * U) {
-    double x[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const long long i = base + k * NT + threadIdx.x;
-      x[k] = i < hi ? __ldcg(src + i) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const long long i = base + k * NT + threadIdx.x;
-      if (i >= hi) continue;
-      double q;
-      if (x[k] == 0.0 && plain) q = 0.0 * rd;        // +-0 / denom, sign kept
-      else if (plain && fabs(x[k]) < 0x1p+900 && fabs(x[k]) > 0x1p-900) q = div_by(x[k], denom, rd);
-      else q = x[k] / denom;
-      st_hint(dst + i, np_min1(q), pol_out);
-    }
-  }
+  stream_chunk(s, src, lo, hi, [&](long long i, double x) {
+    st_hint(dst + i, normalise(x, denom, rd, plain), pol_out);
+  });
 }
 
 // ------------------------------------------------------------- scheduler
-__device__ __forceinline__ long long clampll(long long v, long long lo, long long hi) {
-  return v < lo ? lo : (v > hi ? hi : v);
-}
-__device__ __forceinline__ long long step_start(const Params& p, long long st) {
-  return (long long)p.TE * clampll(st, 0, p.B) + (long long)p.TC * clampll(st - LAG1, 0, p.B) +
-         (long long)p.TA * clampll(st - LAG2, 0, p.B);
+// Thread 0 claims the next task, in priority order: an A chunk of the oldest view whose
+// median is published, a C chunk of the oldest view whose bins are published (and whose
+// candidate ring slot is free), else the next E tile if it is at most AHEAD views past the
+// A front (bounding the L2-resident thinned maps).  A/C work is claimed only when ready, so
+// no task ever waits; TASK_NONE means "nothing ready right now".
+enum TaskKind { TASK_END = 0, TASK_E = 1, TASK_C = 2, TASK_A = 3, TASK_NONE = 4 };
+
+// Optional per-task trace (igs_debug_edge_trace): {start_ns, end_ns, kind, view, idx, smid}.
+struct TraceRec {
+  unsigned long long t0, t1;
+  int kind, view, idx, sm;
+};
+__device__ TraceRec* g_trace = nullptr;
+__device__ unsigned long long g_trace_cap = 0;
+__device__ unsigned long long g_trace_n = 0;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
-enum TaskKind { TASK_END = 0, TASK_E = 1, TASK_C = 2, TASK_A = 3 };
-
-// Thread 0: decode queue index t into (kind, view, index).
-__device__ void decode_task(const Params& p, long long t, int& kind, int& view, int& idx) {
-  if (t >= p.total_tasks) {
-    kind = TASK_END;
+__device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
+  unsigned* sched = p.sched;
+  const unsigned B = (unsigned)p.B;
+  if (p.median) {
+    for (;;) {  // A
+      const unsigned v = ld_acquire(&sched[2]);
+      if (v >= B || !ld_acquire(&p.ctl[v].select_done)) break;
+      const unsigned c = atomicAdd(&p.ctl[v].a_claim, 1u);
+      if (c < (unsigned)p.TA) {
+        kind = TASK_A; view = (int)v; idx = (int)c;
+        return;
+      }
+      atomicCAS(&sched[2], v, v + 1);
+    }
+    for (;;) {  // C
+      const unsigned v = ld_acquire(&sched[1]);
+      if (v >= B || !ld_acquire(&p.ctl[v].binfound)) break;
+      if (v >= (unsigned)RING && !ld_acquire(&p.ctl[v - RING].select_done)) break;
+      const unsigned c = atomicAdd(&p.ctl[v].c_claim, 1u);
+      if (c < (unsigned)p.TC) {
+        kind = TASK_C; view = (int)v; idx = (int)c;
+        return;
+      }
+      atomicCAS(&sched[1], v, v + 1);
+    }
+  }
+  const unsigned long long total_e = (unsigned long long)p.B * p.TE;
+  unsigned long long* e_next = (unsigned long long*)&sched[4];
+  unsigned long long t = ld_acquire64(e_next);
+  // throttle (racy by design: concurrent claimers may overshoot by about one view)
+  if (t < total_e && !(p.median && t / p.TE >= ld_acquire(&sched[2]) + AHEAD)) {
+    t = atomicAdd(e_next, 1ull);  // an atomicAdd never retries, unlike a CAS claim
+    if (t < total_e) {
+      const unsigned v = (unsigned)(t / p.TE);
+      kind = TASK_E; view = (int)v; idx = (int)(t - (unsigned long long)v * p.TE);
+      return;
+    }
+  }
+  if (!p.median) {
+    kind = t >= total_e ? TASK_END : TASK_NONE;
     return;
   }
-  long long lo = 0, hi = p.B + (p.median ? LAG2 : 0);  // step_start(hi) > t
-  while (hi - lo > 1) {
-    const long long mid = (lo + hi) >> 1;
-    if (step_start(p, mid) <= t) lo = mid; else hi = mid;
+  kind = ld_acquire(&sched[2]) >= B ? TASK_END : TASK_NONE;
+}
+
+// L2 prefetch of an E task's input rows, one bulk prefetch per row, issued by thread 0 one
+// task ahead with the input's evict_first policy.
+template <int CH, bool F64>
+__device__ void prefetch_tile(const Params& p, int v, int t, unsigned long long pol) {
+  using T = typename std::conditional<F64, double, float>::type;
+  const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
+  const int H = (int)p.H, W = (int)p.W;
+  const int xl = clamp_i(tx * TW - 4, 0, W - 1), xh = clamp_i(tx * TW + TW + 4, 1, W);
+  const char* base = (const char*)p.img;
+  const unsigned long long total = ((unsigned long long)p.B * p.npx * CH * sizeof(T)) & ~15ull;
+  const int ylo = clamp_i(ty * TH - 4, 0, H - 1), yhi = clamp_i(ty * TH + TH + 4, 1, H);
+  for (int y = ylo; y < yhi; ++y) {
+    const unsigned long long row = (unsigned long long)v * p.npx + (unsigned long long)y * W;
+    unsigned long long a = ((row + xl) * CH * sizeof(T)) & ~15ull;
+    unsigned long long e = ((row + xh) * CH * sizeof(T) + 15) & ~15ull;
+    if (e > total) e = total;
+    if (e <= a) continue;
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(base + a),
+                 "r"((unsigned)(e - a)), "l"(pol)
+                 : "memory");
   }
-  long long off = t - step_start(p, lo);
-  const long long st = lo;
-  if (st < p.B) {
-    if (off < p.TE) {
-      kind = TASK_E; view = (int)st; idx = (int)off;
-      return;
-    }
-    off -= p.TE;
-  }
-  if (st >= LAG1 && st < p.B + LAG1) {
-    if (off < p.TC) {
-      kind = TASK_C; view = (int)(st - LAG1); idx = (int)off;
-      return;
-    }
-    off -= p.TC;
-  }
-  kind = TASK_A; view = (int)(st - LAG2); idx = (int)off;
+}
+
+// Thread 0: claim the next task into s.task_* and warm L2 with its input rows.
+template <int CH, bool F64>
+__device__ void claim_next(const Params& p, Smem& s, unsigned long long pol_in) {
+  int nk = 0, nv = 0, ni = 0;
+  claim_task(p, nk, nv, ni);
+  s.task_kind = nk;
+  s.task_view = nv;
+  s.task_idx = ni;
+  if (nk == TASK_E && p.mode == MODE_FUSED) prefetch_tile<CH, F64>(p, nv, ni, pol_in);
 }
 
 template <bool FAST, int CH, bool F64>
 __global__ void __launch_bounds__(NT, 4) edge_persistent_kernel(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
-  for (int i = threadIdx.x; i < NB; i += NT) s.hist[i] = 0;
+  for (int i = threadIdx.x; i < NB / 2; i += NT) s.hist[i] = 0;
   const unsigned long long pol_in = policy_evict_first();
   const unsigned long long pol_mid = policy_evict_last();
   const unsigned long long pol_out = policy_evict_first();
+  if (threadIdx.x == 0) {
+    int kind = 0, view = 0, idx = 0;
+    claim_task(p, kind, view, idx);
+    s.task_kind = kind;
+    s.task_view = view;
+    s.task_idx = idx;
+  }
   __syncthreads();
+  TraceRec* trace = g_trace;
   for (;;) {
-    if (threadIdx.x == 0) {
-      int kind = 0, view = 0, idx = 0;
-      decode_task(p, (long long)atomicAdd(p.queue, 1ull), kind, view, idx);
-      s.task_kind = kind;
-      s.task_view = view;
-      s.task_idx = idx;
-    }
-    __syncthreads();
     const int kind = s.task_kind, v = s.task_view, idx = s.task_idx;
     __syncthreads();
     if (kind == TASK_END) break;
+    const unsigned long long t_start = trace ? gtimer() : 0ull;
+    // Claim the next task while this one runs: short tasks claim now; a fused tile claims at
+    // the start of its NMS phase, so ready C/A work is not held behind a whole tile.
+    const bool late_claim = kind == TASK_E && p.mode == MODE_FUSED;
+    if (threadIdx.x == 0 && !late_claim) claim_next<CH, F64>(p, s, pol_in);
     if (kind == TASK_E) {
       if (p.mode == MODE_FUSED) run_tile<FAST, CH, F64>(p, s, v, idx, pol_in, pol_mid);
       else run_hist_chunk(p, s, v, idx);
       if (p.median) {
         flush_hist(p, s, v);
-        __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) s.flag = (atomicAdd(&p.ctl[v].tiles_done, 1u) == (unsigned)p.TE - 1);
-        __syncthreads();
-        if (s.flag) {
+        if (threadIdx.x == 0) {
           __threadfence();
-          find_median_bins(p, s, v);
+          s.flag = (atomicAdd(&p.ctl[v].tiles_done, 1u) == (unsigned)p.TE - 1);
+          if (s.flag) __threadfence();
         }
+        __syncthreads();
+        if (s.flag) find_median_bins(p, s, v);
       }
     } else if (kind == TASK_C) {
-      run_collect(p, s, v, idx, pol_mid);
-      __threadfence();
+      run_collect(p, s, v, idx);
       __syncthreads();
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0) {
+        __threadfence();
         s.flag = __ldcg(&p.ctl[v].npos) &&
                  (atomicAdd(&p.ctl[v].collect_done, 1u) == (unsigned)p.TC - 1);
-      __syncthreads();
-      if (s.flag) {
-        __threadfence();
-        run_select(p, s, v);
+        if (s.flag) __threadfence();
       }
-    } else {
+      __syncthreads();
+      if (s.flag) run_select(p, s, v);
+    } else if (kind == TASK_A) {
       run_apply(p, s, v, idx, pol_out);
+    } else if (threadIdx.x == 0) {
+      __nanosleep(1000);
     }
     __syncthreads();
+    if (trace && threadIdx.x == 0) {
+      const unsigned long long k = atomicAdd(&g_trace_n, 1ull);
+      if (k < g_trace_cap) {
+        unsigned sm;
+        asm("mov.u32 %0, %%smid;" : "=r"(sm));
+        trace[k] = TraceRec{t_start, gtimer(), kind, v, idx, (int)sm};
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------- host side
 struct Layout {
-  size_t ctl, hist, hist2, cand, queue, zero_bytes, total;
+  size_t ctl, hist, hist2, slots, cand, queue, zero_bytes, total;
 };
 
 Layout layout(long long B, long long npx, bool median) {
@@ -691,6 +982,8 @@ Layout layout(long long B, long long npx, bool median) {
   L.hist2 = off;
   off = align_up(off + sizeof(unsigned) * 2 * NB2 * (size_t)RING, 256);
   L.zero_bytes = off;
+  L.slots = off;
+  off = align_up(off + sizeof(double) * 2 * NB2 * SLOTS * (size_t)RING, 256);
   L.cand = off;
   if (median) off = align_up(off + sizeof(double) * (size_t)npx * (size_t)(B < RING ? B : RING), 256);
   L.total = off;
@@ -726,12 +1019,13 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   Layout L = layout(p.B, p.npx, median);
   if (ws_bytes < L.total || ws == nullptr) return IGS_ERR_WORKSPACE;
   char* w = (char*)ws;
-  p.queue = (unsigned long long*)(w + L.queue);
+  p.sched = (unsigned*)(w + L.queue);
   p.ctl = (ViewCtl*)(w + L.ctl);
   p.hist = (unsigned*)(w + L.hist);
   p.hist2 = (unsigned*)(w + L.hist2);
   p.cand = (double*)(w + L.cand);
-  IGS_CUDA_TRY(cudaMemsetAsync(w, 0, L.zero_bytes, stream));  // queue, ctl, hist, hist2
+  p.slots = (double*)(w + L.slots);
+  IGS_CUDA_TRY(cudaMemsetAsync(w, 0, L.zero_bytes, stream));  // sched, ctl, hist, hist2
   if (p.mode == MODE_FUSED) {
     p.tiles_x = (int)((p.W + TW - 1) / TW);
     p.tiles_y = (int)((p.H + TH - 1) / TH);
@@ -741,7 +1035,6 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   }
   p.TC = median ? (int)((p.npx + CHUNK - 1) / CHUNK) : 0;
   p.TA = p.TC;
-  p.total_tasks = (long long)(p.TE + p.TC + p.TA) * p.B;
   const bool fast = p.sym && !p.skip;
   KernelFn fn = nullptr;
   int bps = 0;
@@ -752,7 +1045,8 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   else fast ? pick<true, 1, false>(fn, bps) : pick<false, 1, false>(fn, bps);
   if (bps <= 0) return IGS_ERR_CUDA;
   long long grid = (long long)bps * sm_count();
-  if (grid > p.total_tasks) grid = p.total_tasks;
+  const long long total_tasks = (long long)(p.TE + p.TC + p.TA) * p.B;
+  if (grid > total_tasks) grid = total_tasks;
   if (grid < 1) grid = 1;
   void* args[] = {&p};
   IGS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fn, dim3((unsigned)grid), dim3(NT), args,
@@ -896,6 +1190,23 @@ int igs_edge_importance(const void* image, int in_dtype, int channels, int64_t b
   p.out = out;
   edge::set_weights(p, blur_w25);
   return edge::launch(p, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+// Debug: trace every task of subsequent igs_edge_importance launches into buf (device memory,
+// capacity records of 32 bytes); buf == NULL disables.  Returns the records written so far
+// (of the previous launches) in *written when non-NULL.
+int igs_debug_edge_trace(void* buf, int64_t capacity, int64_t* written) {
+  if (written) {
+    unsigned long long n = 0;
+    IGS_CUDA_TRY(cudaMemcpyFromSymbol(&n, edge::g_trace_n, sizeof(n)));
+    *written = (int64_t)n;
+  }
+  edge::TraceRec* p = (edge::TraceRec*)buf;
+  unsigned long long cap = buf ? (unsigned long long)capacity : 0ull, zero = 0;
+  IGS_CUDA_TRY(cudaMemcpyToSymbol(edge::g_trace, &p, sizeof(p)));
+  IGS_CUDA_TRY(cudaMemcpyToSymbol(edge::g_trace_cap, &cap, sizeof(cap)));
+  IGS_CUDA_TRY(cudaMemcpyToSymbol(edge::g_trace_n, &zero, sizeof(zero)));
+  return IGS_OK;
 }
 
 int igs_median_normalize(const double* in, int64_t batch, int64_t n, double* out,

@@ -37,6 +37,12 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
   while (ld_acquire(p) < target) __nanosleep(64);
 }
@@ -163,6 +169,18 @@ __device__ __forceinline__ double hypot_glibc_fast(double x, double y) {
   }
   // common case first: 2^-459 <= ay, ax <= 2^511 and ay > ax * 2^-54
   if (ay >= 0x1p-459 && ax <= 0x1p+511 && ay > ax * 0x1p-54) return hypot_kernel_fast(ax, ay);
+  return hypot_glibc(x, y);
+}
+
+// Same for |x|, |y| <= 2^511 (Sobel of an RGB-derived gray in [0, 1]: |g| <= 4).
+__device__ __forceinline__ double hypot_glibc_fast_bounded(double x, double y) {
+  double ax = fabs(x), ay = fabs(y);
+  if (ax < ay) {
+    double t = ax;
+    ax = ay;
+    ay = t;
+  }
+  if (ay >= 0x1p-459 && ay > ax * 0x1p-54) return hypot_kernel_fast(ax, ay);
   return hypot_glibc(x, y);
 }
 
