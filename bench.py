@@ -357,13 +357,15 @@ def bench_las(args, world, dev, peak, peak_src):
         if it >= args.warmup:
             dsteps.append(a.elapsed_time(c))
     ds_ms = max_over_ranks(statistics.median(dsteps), world)
+    las_traffic = ncu_traffic().get("las_apply_kernel_bytes_per_split")
     res = {"metric": "LAS Gaussians/s", "value": round(world * n / (ms * 1e-3), 1),
            "unit": "Gaussians/s", "ms_per_step": round(ms, 4),
            "config": {"workload": "las_split_batch, 1M Gaussians all masked, SH degree 3 "
                                   "(59 fp32/Gaussian), capacity 2M (BASELINE.json configs[2])",
                       "l2": "500 MB moved per step >> L2"},
            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                        "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                        "unit": "GB/s", "frac": round(achieved / peak, 4),
+                        "traffic": (round(las_traffic * n) if las_traffic else None),
                         "kernel": "las_apply_kernel", "algorithmic_bytes_per_split": 500,
                         "apply_ms": round(ms_apply, 4), "peak_source": peak_src},
            "densify_step": {"ms": round(ds_ms, 4), "n": n, "split": ev.split,

@@ -110,6 +110,34 @@ int igs_select_candidates(const double* grad_sum, int64_t accum_count, const dou
                           int64_t take_cap, uint8_t* mask, int64_t* counts,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- sharded selection (multi-GPU) ---------------------- *
+ * The same result as igs_select_candidates over the concatenation of every rank's
+ * contiguous shard (densify_controller.py:80-106 on the global arrays), split into the
+ * per-rank launches of a radix select whose merge steps are collectives the caller issues
+ * on the same stream (torch.distributed / NCCL):
+ *   igs_select_shard_keys                 -> all-reduce(sum) hist
+ *   igs_select_shard_resolve(round 0)
+ *   for round 1..3: igs_select_shard_hist -> all-reduce(sum) hist; igs_select_shard_resolve
+ *   igs_select_shard_ties                 -> all-gather local_ties (one int64 per rank)
+ *   igs_select_shard_finalize
+ * hist is a device int32[IGS_SHARD_HIST_LEN] buffer: 65536 digit bins, then the eligible
+ * count (round 0).  take_cap is computed on the host from the GLOBAL count and headroom
+ * (:99-100).  counts (device int64[2], nullable) receives the global {#eligible, take}. */
+#define IGS_SHARD_HIST_LEN 65537
+int igs_select_shard_workspace_bytes(int64_t n, size_t* bytes);
+int igs_select_shard_keys(const double* grad_sum, int64_t accum_count, const double* edge_score,
+                          int64_t n, double grad_threshold, int warmup, int policy, int32_t* hist,
+                          void* workspace, size_t workspace_bytes, void* stream);
+int igs_select_shard_resolve(const int32_t* global_hist, int round, int64_t take_cap,
+                             void* workspace, size_t workspace_bytes, int64_t* counts,
+                             void* stream);
+int igs_select_shard_hist(int64_t n, int round, int32_t* hist, void* workspace,
+                          size_t workspace_bytes, void* stream);
+int igs_select_shard_ties(int64_t n, int64_t* local_ties, void* workspace, size_t workspace_bytes,
+                          void* stream);
+int igs_select_shard_finalize(int64_t n, const int64_t* all_ties, int rank, uint8_t* mask,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- Long-Axis-Split (las_split.py:146-179) ----------------------------- */
 
 int igs_las_workspace_bytes(int64_t count, size_t* bytes);

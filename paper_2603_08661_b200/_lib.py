@@ -20,6 +20,7 @@ IGS_F32, IGS_F64 = 0, 1
 IGS_EDGE_NO_NMS, IGS_EDGE_NO_MEDIAN = 1, 2
 IGS_POLICY = {"product": 0, "edge": 1, "grad": 2}
 IGS_LAS_BAD_QUAT, IGS_LAS_BAD_OPACITY, IGS_LAS_RENORM = 1, 2, 4
+IGS_SHARD_HIST_LEN = 65537  # include/igs_b200.h
 
 _vp, _i64, _sz, _int, _dbl, _flt = C.c_void_p, C.c_int64, C.c_size_t, C.c_int, C.c_double, C.c_float
 _szp = C.POINTER(C.c_size_t)
@@ -42,6 +43,12 @@ SIGNATURES = {
     "igs_select_workspace_bytes": (_int, [_i64, _szp]),
     "igs_select_candidates": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _i64, _vp, _vp, _vp,
                                      _sz, _vp]),
+    "igs_select_shard_workspace_bytes": (_int, [_i64, _szp]),
+    "igs_select_shard_keys": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _vp, _vp, _sz, _vp]),
+    "igs_select_shard_resolve": (_int, [_vp, _int, _i64, _vp, _sz, _vp, _vp]),
+    "igs_select_shard_hist": (_int, [_i64, _int, _vp, _vp, _sz, _vp]),
+    "igs_select_shard_ties": (_int, [_i64, _vp, _vp, _sz, _vp]),
+    "igs_select_shard_finalize": (_int, [_i64, _vp, _int, _vp, _vp, _sz, _vp]),
     "igs_las_workspace_bytes": (_int, [_i64, _szp]),
     "igs_las_prepare": (_int, [_vp, _vp, _vp, _i64, _flt, _vp, _sz, _vp, _vp]),
     "igs_las_apply": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt, _flt,
