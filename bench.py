@@ -13,9 +13,10 @@ densify_step (select 50k of 1M + LAS).
 Multi-GPU (torchrun, one rank per GPU): views shard per GPU (weak scaling, no
 collective on the data path); value = all ranks' pixels / max-over-ranks time.
 
---impl reference: the reference's CPU path on this host -- the oracle port of
-splitkit.edge_pipeline (numpy/scipy-order restatement, oracle/edge.py) over a pool of
-all host cores, one view per process per step; rank 0 only.
+--impl reference: the reference's CPU path on this host -- the unmodified
+splitkit.edge_pipeline.importance_pipeline installed in baseline/_ref (else the oracle
+restatement oracle/edge.py) over a pool of all host cores, one view per process per step;
+rank 0 only.
 """
 
 from __future__ import annotations
@@ -137,25 +138,46 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-# ------------------------------------------------------------------ CPU reference (oracle)
+# ------------------------------------------------------------------ CPU reference
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")  # the unmodified splitkit
+
+
+def ref_kind():
+    """"reference" when the unmodified splitkit is installed in baseline/_ref (it travels to
+    the GPU box with the snapshot), else "port" (the oracle restatement)."""
+    return "reference" if os.path.isdir(os.path.join(REF_PATH, "splitkit")) else "port"
+
+
+def ref_edge_fn():
+    if ref_kind() == "reference":
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        from splitkit.edge_pipeline import importance_pipeline
+        return importance_pipeline
+    from oracle import edge as OE
+    return OE.importance_pipeline
+
+
 _CPU_VIEW = None
+_CPU_FN = None
 
 
 def _cpu_init(seed):
-    global _CPU_VIEW
+    global _CPU_VIEW, _CPU_FN
     from paper_2603_08661_b200.synth import synth_view
     _CPU_VIEW = synth_view(H, W, seed + os.getpid() % 97)
+    _CPU_FN = ref_edge_fn()
 
 
 def _cpu_task(_):
-    from oracle import edge as OE
     t0 = time.perf_counter()
-    OE.importance_pipeline(_CPU_VIEW)
+    _CPU_FN(_CPU_VIEW)
     return time.perf_counter() - t0
 
 
 def cpu_edge_rate(steps, warmup, procs=None):
-    """Oracle edge pipeline over a process pool (1 view per process per step) -> MPix/s."""
+    """Reference edge pipeline over a process pool of all host cores (one 1237x822 view per
+    process per step) -> (MPix/s, processes, seconds per step)."""
     import multiprocessing as mp
     procs = procs or len(os.sched_getaffinity(0))
     ctx = mp.get_context("spawn")
@@ -170,19 +192,34 @@ def cpu_edge_rate(steps, warmup, procs=None):
 
 
 def cpu_las_rate(n=200_000):
-    from oracle import las as OL
-    from paper_2603_08661_b200.synth import random_cloud
+    """Reference las_split_batch, all masked, 1 core.  The reference Scene3 holds 3-float
+    colours (core.py:172), so its LAS moves 56 B per record, not the 236 B SH3 record."""
     import numpy as np
+    from paper_2603_08661_b200.synth import random_cloud
     pos, ls, q, o, sh = random_cloud(n, 16, seed=101)
+    mask = np.ones(n, bool)
+    reps = 3
+    if ref_kind() == "reference":
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        from splitkit.core import Scene3
+        from splitkit.las_split import las_split_batch
+        scenes = [Scene3(pos, ls, q, o, sh[:, 0, :], capacity=2 * n) for _ in range(reps + 1)]
+        las_split_batch(scenes[0], mask)
+        t0 = time.perf_counter()
+        for k in range(reps):
+            las_split_batch(scenes[k + 1], mask)
+        return n * reps / (time.perf_counter() - t0), "reference", \
+            f"{reps} x {n // 1000}k all-masked, splitkit.las_split_batch (colour-only records)"
+    from oracle import las as OL
     d = {"positions": pos, "log_scales": ls, "rotations": q, "opacity_logits": o, "sh": sh,
          "capacity": 2 * n}
-    mask = np.ones(n, bool)
     OL.las_split_batch(d, mask)
     t0 = time.perf_counter()
-    reps = 3
     for _ in range(reps):
         OL.las_split_batch(d, mask)
-    return n * reps / (time.perf_counter() - t0)
+    return n * reps / (time.perf_counter() - t0), "port", \
+        f"{reps} x {n // 1000}k all-masked, SH degree 3, oracle/las.py"
 
 
 def run_reference(args, world, rank):
@@ -199,9 +236,12 @@ def run_reference(args, world, rank):
         "config": {"workload": "200 x 1237x822 RGB f64 views: gray+blur+Sobel+NMS+median "
                                "(BASELINE.json configs[1])", "views_per_gpu": VIEWS,
                    "height": H, "width": W},
-        "cpu_baseline": {"value": round(rate, 3), "unit": "MPix/s", "cores": procs, "kind": "port",
-                         "sample": f"{procs} views per step (1 per process), oracle/edge.py "
-                                   "numpy restatement of splitkit.edge_pipeline"},
+        "cpu_baseline": {"value": round(rate, 3), "unit": "MPix/s", "cores": procs,
+                         "kind": ref_kind(),
+                         "sample": f"{procs} views per step (1 per process), "
+                                   + ("splitkit.edge_pipeline.importance_pipeline (baseline/_ref)"
+                                      if ref_kind() == "reference" else
+                                      "oracle/edge.py restatement of splitkit.edge_pipeline")},
         "e2e": {"value": round(rate, 3), "unit": "MPix/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -265,9 +305,11 @@ def run_ours(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, procs, _ = cpu_edge_rate(2, 1)
         line["cpu_baseline"] = {"value": round(rate, 3), "unit": "MPix/s", "cores": procs,
-                                "kind": "port",
-                                "sample": f"3x{procs} views (1 per process per step), "
-                                          "oracle/edge.py on the host cores"}
+                                "kind": ref_kind(),
+                                "sample": f"2x{procs} views (1 per process per step), "
+                                          + ("splitkit importance_pipeline (baseline/_ref)"
+                                             if ref_kind() == "reference" else "oracle/edge.py")
+                                          + " on the host cores"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -373,10 +415,9 @@ def bench_las(args, world, dev, peak, peak_src):
                             "note": "select (radix top-k, take=ceil(0.05 N)) + LAS + one host "
                                     "sync, public densify_step()"}}
     if world == 1 and not args.no_cpu:
-        rate = cpu_las_rate()
+        rate, kind, sample = cpu_las_rate()
         res["cpu_baseline"] = {"value": round(rate, 1), "unit": "Gaussians/s", "cores": 1,
-                               "kind": "port", "sample": "3 x 200k all-masked, SH degree 3, "
-                                                         "oracle/las.py"}
+                               "kind": kind, "sample": sample}
     return res
 
 

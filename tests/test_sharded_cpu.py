@@ -1,0 +1,182 @@
+"""Multi-rank protocol of the sharded densification path on CPU: world_size 2 (and 3) over
+gloo, the per-rank kernels replaced by a numpy test double (tests/shard_double.py).
+Checks that the collective schedule of sharded.select_shard_protocol reproduces the
+single-process oracle selection bit-for-bit, and the host-side global checks / gather."""
+
+import os
+import socket
+import types
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+from oracle import select as OS
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cases, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from shard_double import NumpyShardOps
+
+        from paper_2603_08661_b200 import sharded
+        from paper_2603_08661_b200.densify_controller import DensifyStats
+        from paper_2603_08661_b200.schedule import DensifyConfig
+        for ci, case in enumerate(cases):
+            q.put((ci,) + _one(rank, world, case, sharded, DensifyStats, DensifyConfig,
+                               NumpyShardOps))
+    finally:
+        dist.destroy_process_group()
+
+
+def _one(rank, world, case, sharded, DensifyStats, DensifyConfig, NumpyShardOps):
+    from paper_2603_08661_b200.densify_controller import _take_cap
+    grad, edge, step, policy, cap, headroom = case
+    n = len(grad)
+    lo, hi = sharded.shard_range(n, rank, world)
+    st = DensifyStats(hi - lo, device="cpu")
+    st._grad_sum.copy_(torch.from_numpy(grad[lo:hi] * 2))
+    st._accum_count = 2
+    st.edge_score.copy_(torch.from_numpy(edge[lo:hi]))
+    cfg = DensifyConfig(budget=10 * n, growth_cap=cap, policy=policy)
+    comm = sharded.Comm()
+    take_cap = _take_cap(cfg, n, headroom) if headroom > 0 else 0
+    mask, counts = sharded.select_shard_protocol(NumpyShardOps(hi - lo), st, cfg, step,
+                                                 take_cap, comm)
+    m = torch.zeros(n, dtype=torch.uint8)
+    m[lo:hi] = mask.to(torch.uint8)
+    dist.all_reduce(m)
+    return (rank, m.numpy().astype(bool), counts.tolist())
+
+
+_RESULTS = {}
+
+
+def _run(world, cases):
+    if world not in _RESULTS:
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        res = [q.get(timeout=300) for _ in range(world * len(cases))]
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        _RESULTS[world] = res
+    return _RESULTS[world]
+
+
+CASES = []
+_rng = np.random.default_rng(5)
+for _n, _tied in ((1001, False), (4000, True), (17, True)):
+    g = _rng.exponential(2e-4, _n)
+    e = _rng.random(_n)
+    if _tied:
+        g, e = np.round(g, 4), np.round(e, 1)
+    CASES.append((g, e, 2000, "product", 0.05, _n))
+    CASES.append((g, e, 500, "product", 0.3, _n // 3))
+    CASES.append((g, e, 2000, "grad", 1.0, _n))
+# all ties and no eligible
+CASES.append((np.full(999, 3e-4), np.full(999, 0.5), 2000, "product", 0.5, 999))
+CASES.append((np.full(50, 1e-6), np.full(50, 0.5), 2000, "product", 0.5, 50))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("ci", range(len(CASES)))
+def test_sharded_select_protocol_matches_single_process(world, ci):
+    grad, edge, step, policy, cap, headroom = CASES[ci]
+    res = [r[1:] for r in _run(world, CASES) if r[0] == ci]
+    assert len(res) == world
+    warm = OS.is_warmup_step(500, 15000, 500, 3, step)
+    want, elig = OS.select_candidates(OS.grad_norm(grad * 2, 2), edge, warm, policy, 2e-4, cap,
+                                      headroom)
+    for rank, mask, counts in res:
+        np.testing.assert_array_equal(mask, want, err_msg=f"rank {rank}")
+        assert counts[0] == elig
+        assert counts[1] == int(want.sum())
+
+
+def test_shard_range_covers_contiguously():
+    from paper_2603_08661_b200.sharded import shard_range
+    for n in (0, 1, 7, 8, 1000, 6_000_001):
+        for world in (1, 2, 3, 8):
+            parts = [shard_range(n, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            sizes = [h - l for l, h in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+def test_global_las_checks():
+    from paper_2603_08661_b200 import _lib, sharded
+    from paper_2603_08661_b200.las_split import BudgetError, SplitConstants
+    c = SplitConstants()
+    caps = [(10, 20), (10, 12)]
+    assert sharded._las_check_global(None, [(5, 0), (2, 0)], caps, c) == 0
+    with pytest.raises(BudgetError):
+        sharded._las_check_global(None, [(5, 0), (3, 0)], caps, c)
+    # renormalisation is batch-global: one rank's flag applies to every rank
+    assert sharded._las_check_global(None, [(1, _lib.IGS_LAS_RENORM), (1, 0)], caps, c) == \
+        _lib.IGS_LAS_RENORM
+    # flags of a rank that splits nothing do not count (its masked batch is empty)
+    assert sharded._las_check_global(None, [(0, _lib.IGS_LAS_BAD_QUAT), (1, 0)], caps, c) == 0
+    with pytest.raises(ValueError):
+        sharded._las_check_global(None, [(1, _lib.IGS_LAS_BAD_QUAT), (1, 0)], caps, c)
+
+
+def _gather_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_08661_b200 import sharded
+        # rank r holds parents [r*10, r*10 + 3 + r) then 2 appended children
+        parents = 3 + rank
+        n = parents + 2
+        rows = torch.arange(n, dtype=torch.float32) + 100 * rank
+        sc = types.SimpleNamespace(
+            _pos=rows[:, None].repeat(1, 3), _ls=rows[:, None].repeat(1, 3),
+            _rot=rows[:, None].repeat(1, 4), _op=rows.clone(),
+            _sh=rows[:, None, None].repeat(1, 2, 3), count=n, device=torch.device("cpu"))
+        out = sharded.gather_scene(sc, parents, sharded.Comm())
+        q.put((rank, out["opacity_logits"].numpy().tolist(), tuple(out["sh"].shape)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_scene_reference_layout():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [0, 1, 2, 100, 101, 102, 103, 3, 4, 104, 105]
+    for rank, op, shape in res:
+        assert op == want
+        assert shape == (11, 2, 3)

@@ -1,0 +1,126 @@
+"""GPU parity of the sharded densification path (igs_select_shard_* + las on shards).
+
+* world 1 (no process group): the sharded radix select through the real CUDA kernels equals
+  the single-launch select and the oracle, bit for bit;
+* world 2 over gloo, both ranks on cuda:0 (the box has one GPU; NCCL refuses two ranks per
+  device): densify_step_sharded + gather_scene reproduce the single-device densify_step
+  exactly (masks, counts, every column in the reference's global layout)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+from oracle import select as OS
+
+pytestmark = pytest.mark.gpu
+
+
+def _stats(b, grad_sum, accum, edge, device="cuda"):
+    st = b.DensifyStats(len(grad_sum), device=device)
+    st._grad_sum.copy_(torch.from_numpy(np.asarray(grad_sum, np.float64)))
+    st._accum_count = int(accum)
+    st.set_edge_score(edge)
+    return st
+
+
+@pytest.mark.parametrize("n", [1, 5, 3000, 65_536 * 3 + 7, 750_000])
+@pytest.mark.parametrize("tied", [False, True])
+def test_world1_sharded_select_equals_single(n, tied):
+    import paper_2603_08661_b200 as b
+    from paper_2603_08661_b200 import sharded
+    rng = np.random.default_rng(n * 2 + tied)
+    grad, edge = rng.exponential(2e-4, n), rng.random(n)
+    if tied:
+        grad, edge = np.round(grad, 4), np.round(edge, 1)
+    for step, policy, cap in ((2000, "product", 0.05), (500, "edge", 0.3), (2000, "grad", 1.0)):
+        cfg = b.DensifyConfig(budget=10 * n, growth_cap=cap, policy=policy)
+        st = _stats(b, grad * 3, 3, edge)
+        got = sharded.select_candidates_sharded(st, cfg, step, n, n).cpu().numpy()
+        single = b.select_candidates(st, cfg, step, n).cpu().numpy()
+        warm = OS.is_warmup_step(500, 15000, 500, 3, step)
+        want, _ = OS.select_candidates(OS.grad_norm(grad * 3, 3), edge, warm, policy, 2e-4, cap, n)
+        np.testing.assert_array_equal(got, want)
+        np.testing.assert_array_equal(single, want)
+
+
+def test_world1_order_semantics():
+    import paper_2603_08661_b200 as b
+    from paper_2603_08661_b200 import sharded
+    edge = np.array([0.5, np.nan, -0.0, 0.0, 0.5, np.inf, 0.25])
+    cfg = b.DensifyConfig(budget=100, growth_cap=1.0, policy="edge")
+    for take in range(1, 8):
+        st = _stats(b, np.ones(7), 1, edge)
+        got = sharded.select_candidates_sharded(st, cfg, 500, take, 7).cpu().numpy()
+        want, _ = OS.select_candidates(np.ones(7), edge, True, "edge", 2e-4, 1.0, take)
+        np.testing.assert_array_equal(got, want)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cloud(n, seed):
+    from paper_2603_08661_b200.synth import random_cloud
+    return random_cloud(n, 16, seed=seed)
+
+
+def _worker(rank, world, port, n, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2603_08661_b200 as b
+        from paper_2603_08661_b200 import sharded
+        pos, ls, qq, o, sh = _cloud(n, 11)
+        rng = np.random.default_rng(12)
+        grad, edge = rng.exponential(3e-4, n), np.round(rng.random(n), 2)
+        lo, hi = sharded.shard_range(n, rank, world)
+        k = hi - lo
+        scene = b.Scene3(pos[lo:hi], ls[lo:hi], qq[lo:hi], o[lo:hi], sh[lo:hi], capacity=2 * k)
+        st = _stats(b, grad[lo:hi], 1, edge[lo:hi])
+        cfg = b.DensifyConfig(budget=2 * n, growth_cap=0.3)
+        ev = sharded.densify_step_sharded(scene, st, cfg, 2000)
+        full = sharded.gather_scene(scene, k)
+        q.put((rank, (ev.step, ev.eligible, ev.split, ev.count_after),
+               {kk: v.cpu().numpy() for kk, v in full.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_gloo_densify_step_matches_single_device():
+    import paper_2603_08661_b200 as b
+    n = 20_001
+    pos, ls, qq, o, sh = _cloud(n, 11)
+    rng = np.random.default_rng(12)
+    grad, edge = rng.exponential(3e-4, n), np.round(rng.random(n), 2)
+    scene = b.Scene3(pos, ls, qq, o, sh, capacity=2 * n)
+    st = _stats(b, grad, 1, edge)
+    cfg = b.DensifyConfig(budget=2 * n, growth_cap=0.3)
+    ev = b.densify_step(scene, st, cfg, 2000)
+    want = scene.to_numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, evt, full in res:
+        assert evt == (ev.step, ev.eligible, ev.split, ev.count_after), rank
+        for col in ("positions", "log_scales", "rotations", "opacity_logits", "sh"):
+            np.testing.assert_array_equal(full[col], want[col], err_msg=f"{col} rank {rank}")
