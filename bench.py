@@ -302,6 +302,7 @@ def run_ours(args, world, rank, local):
         line["e2e"] = e2e_edge(args, world, dev)
     if not args.no_las:
         line["las"] = bench_las(args, world, dev, peak, peak_src)
+        line["densify_sharded"] = bench_densify_sharded(args, world, rank, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, procs, _ = cpu_edge_rate(2, 1)
         line["cpu_baseline"] = {"value": round(rate, 3), "unit": "MPix/s", "cores": procs,
@@ -419,6 +420,63 @@ def bench_las(args, world, dev, peak, peak_src):
         res["cpu_baseline"] = {"value": round(rate, 1), "unit": "Gaussians/s", "cores": 1,
                                "kind": kind, "sample": sample}
     return res
+
+
+DENSIFY_N = 6_000_000
+
+
+def bench_densify_sharded(args, world, rank, dev):
+    """BASELINE.json configs[3]: the full densify step on a 6M-Gaussian SH3 cloud split in
+    contiguous shards over the ranks (strong scaling: 6M total at every N).  One step =
+    sharded select (4 histogram all-reduces + 1 tie all-gather over NCCL) + sharded LAS
+    (1 all-gather of counts/flags) + the host reads; max over ranks of the median step."""
+    import torch
+
+    import paper_2603_08661_b200 as igs
+    from paper_2603_08661_b200 import sharded
+    from paper_2603_08661_b200.synth import random_cloud_torch, random_stats
+
+    lo, hi = sharded.shard_range(DENSIFY_N, rank, world)
+    k = hi - lo
+    pos, ls, q, o, sh = random_cloud_torch(k, 16, seed=301 + rank, device=dev)
+    scene = igs.Scene3(pos, ls, q, o, sh, capacity=2 * k, device=dev)
+    pristine = {name: getattr(scene, name)[:k].clone() for name in ("_pos", "_ls", "_op")}
+    grad, edge = random_stats(k, seed=17 + rank)
+    grad_t = torch.from_numpy(grad).to(dev)
+    comm = sharded.Comm()
+    caps = sharded.global_counts(scene, comm)
+    cfg = igs.DensifyConfig(budget=2 * DENSIFY_N)
+    times, ev = [], None
+    steps = max(3, min(args.steps, 20))
+    for it in range(args.warmup + steps):
+        for name, v in pristine.items():
+            getattr(scene, name)[:k].copy_(v)
+        scene._set_count(k)
+        stats = igs.DensifyStats(k, device=dev)
+        stats._grad_sum.copy_(grad_t)
+        stats._accum_count = 1
+        stats.set_edge_score(edge)
+        torch.cuda.synchronize()
+        barrier(world)
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ev = sharded.densify_step_sharded(scene, stats, cfg, 2000, comm, caps=caps)
+        c.record()
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            times.append(a.elapsed_time(c))
+    ms = max_over_ranks(statistics.median(times), world)
+    algo = DENSIFY_N * 17 + ev.split * 500  # select bytes + LAS bytes (SURVEY.md 8(d))
+    return {"metric": "densify step Gaussians/s", "value": round(DENSIFY_N / (ms * 1e-3), 1),
+            "unit": "Gaussians/s", "ms_per_step": round(ms, 4), "scaling": "strong",
+            "n_gpus": world, "split": ev.split, "eligible": ev.eligible,
+            "count_after": ev.count_after,
+            "algorithmic_GBps_per_gpu": round(algo / world / (ms * 1e-3) / 1e9, 1),
+            "config": {"workload": "densify_step_sharded on a 6M-Gaussian SH3 cloud, contiguous "
+                                   f"shards of {k} per GPU, take = ceil(0.05 N) = 300k "
+                                   "(BASELINE.json configs[3])",
+                       "collectives": "4 x 256 KB all-reduce + 2 small all-gathers per step "
+                                      + ("(NCCL)" if world > 1 else "(none at N=1)")}}
 
 
 def main():

@@ -4,9 +4,10 @@
 // (/root/reference/pkg/src/splitkit/edge_pipeline.py:42-135).
 //
 // Task kinds (one persistent cooperative grid, 256-thread blocks):
-//   E(v,t)  fused tile: gray -> 5x5 blur -> Sobel -> |g| + direction bin -> NMS
-//           for a TH x TW output tile staged in shared memory with a 4-pixel
-//           halo; writes the thinned map and merges a per-view histogram of the
+//   E(v,t)  fused band: gray -> 5x5 blur -> Sobel -> direction bin -> NMS over a
+//           band of <= 124 columns x <= 128 rows, walked top to bottom in 16-row
+//           sub-steps with the context rows kept in shared memory (see run_band);
+//           writes the thinned map and merges a per-view histogram of the
 //           positive survivors.  The last E task of a view locates the median
 //           histogram bin(s).                                 (:42-114, :123)
 //   C(v,c)  collect: gathers the values falling in the median bin(s) into a
@@ -16,19 +17,21 @@
 //   A(v,c)  apply: out = min(v / (2 m), 1) in place.                     (:125)
 // Scheduling is dependency driven (claim_task): A work of views whose median is
 // published first, then C work of views whose bins are published, else the next
-// E tile -- at most AHEAD views past the A front, so only a few views' thinned
+// E band -- at most `ahead` views past the A front, so only a few views' thinned
 // maps are live.  Those are stored with an L2 evict_last policy (the input
 // streams with evict_first), so E, C and A meet in L2 and the final map is
 // written back to HBM once.  Work is claimed only when ready: no task waits.
 //
 // Arithmetic: float64 in scipy's order (see oracle/edge.py): taps summed in
 // row-major order from 0.0 with separately rounded multiply and add; glibc's
-// hypot; the NMS direction bin from exact comparisons against tan(pi/8) with a
-// fallback to numpy's floor((mod(atan2)+pi/8)/(pi/4)) within 1e-12 rad of a
-// boundary.
+// hypot (exact, IEEE division) for every stored magnitude; the NMS compares
+// ordered by |g|^2 keys with an exact-hypot fallback (see band_nms); the NMS direction
+// bin from exact comparisons against tan(pi/8) with a fallback to numpy's
+// floor((mod(atan2)+pi/8)/(pi/4)) within 1e-12 rad of a boundary.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <type_traits>
@@ -38,16 +41,17 @@
 namespace igs {
 namespace edge {
 
-constexpr int TH = 32, TW = 60;              // output tile
-constexpr int MH = TH + 2, MW = TW + 2;      // gradient magnitude region (NMS halo 1)
-constexpr int BH = TH + 4, BW = TW + 4;      // blurred region (Sobel halo 1)
-constexpr int GH = TH + 8, GW = TW + 8;      // gray region (blur halo 2)
 constexpr int NT = 256;                      // threads per block
 constexpr int NWARP = NT / 32;
-constexpr int SB = 9;                        // blur strip height: BW x (BH/SB) = 256 strips
-static_assert(BW * (BH / SB) == NT && BH % SB == 0, "blur strips must cover the block");
-static_assert(MH * MW <= GH * GW, "magnitude aliases the gray buffer");
-static_assert(GW <= 96, "phase A covers a row with three lanes per warp lane");
+constexpr int SR = 16;                       // output rows per band sub-step
+constexpr int TWM = 124;                     // max output columns per band
+constexpr int BAND_H = 128;                  // max rows per band
+constexpr int GWP = TWM + 8, BWP = 128, MWP = 128;  // row pitches (cells); the blur /
+                                                    // Sobel lanes cover 128 columns
+constexpr int GR = SR + 8, BR = SR + 4, QR = SR + 2;        // rows per sub-step + context
+static_assert(TWM * BAND_H < 65536, "16-bit shared histogram counters per band");
+static_assert(TWM + 4 <= 128 && 2 * 8 == SR, "blur / Sobel: 128 columns x 2 strips of 8 rows");
+static_assert(TWM + 8 <= 132, "gray: 4 x 32 lanes + 4 columns");
 
 constexpr int NB = 4096;                     // level-1 median histogram: 64 bins per octave
 constexpr int HIST_SHIFT = 46;               // bin = (bits >> 46) - HIST_BASE (18 top bits)
@@ -57,9 +61,8 @@ constexpr int SUB_SHIFT = 34;                // level-2 bin = bits 45..34 inside
 constexpr int SLOTS = 8;                     // candidates kept per level-2 bin
 constexpr int NB2 = 4096;                    // level-2 histogram: bits 47..36 inside a bin
 constexpr int CHUNK = 16384;                 // pixels per collect/apply task (< 65536)
-constexpr int AHEAD = 5;                     // E may run at most AHEAD views past the A front
-constexpr int RING = AHEAD + 2;              // candidate buffers / level-2 histograms in flight
-constexpr int SEL_CAP = (GH * GW + BH * BW); // doubles of smem the select may use
+constexpr int RING = 12;                     // candidate buffers / level-2 histograms in flight
+constexpr int SEL_CAP = GR * GWP + BR * BWP;  // doubles of smem the select may use
 
 enum Mode { MODE_FUSED = 0, MODE_MEDIAN_ONLY = 1 };
 
@@ -96,7 +99,10 @@ struct Params {
   double* out;              // (B, npx) float64
   double* medians;          // optional (B,) output of the medians
   // scheduling
-  int tiles_x, tiles_y, TE, TC, TA;
+  int tw, ncols, band_h, TE, TC, TA;
+  int ahead;                // E may run at most `ahead` views past the A front (< RING)
+  double kgray[3];          // Rec.601 weights (edge_pipeline.py:22), in the constant bank
+  double ktan, ktol;        // tan(pi/8) and the 1e-12 relative margin of the direction bin
   // workspace
   unsigned* sched;          // [1] C front view, [2] A front view, [4..5] next E task (u64)
   ViewCtl* ctl;
@@ -107,9 +113,11 @@ struct Params {
 };
 
 struct __align__(16) Smem {
-  double g[GH * GW];        // gray, then gradient magnitude; select scratch
-  double b[BH * BW];        // blurred; select scratch (contiguous with g)
-  uint8_t bin[TH * TW];     // NMS direction bins of the output tile
+  double g[GR * GWP];       // gray rows of a band sub-step; C/A stream buffers, select scratch
+  double b[BR * BWP];       // blurred rows (contiguous with g)
+  unsigned q[QR * MWP];     // Sobel cells: (|grad|^2 key << 2) | direction bin
+  unsigned list[SR * TWM];  // compacted NMS survivors / undecided pixels of a sub-step
+  unsigned list_n[2];       // list lengths (double-buffered by sub-step parity)
   unsigned hist[NB / 2];    // level-1 counts packed two 16-bit bins per word; radix scratch
   unsigned warp_sums[32];
   int task_kind, task_view, task_idx, flag;
@@ -183,7 +191,6 @@ __device__ __forceinline__ long long clampi(long long v, long long lo, long long
   return v < lo ? lo : (v > hi ? hi : v);
 }
 
-__device__ __forceinline__ int y0_row(int ty, int r, int H) { return clamp_i(ty * TH - 4 + r, 0, H - 1); }
 
 __device__ __forceinline__ int hist_bin(double v) {
   long long hb = (long long)((unsigned long long)__double_as_longlong(v) >> HIST_SHIFT) - HIST_BASE;
@@ -195,191 +202,395 @@ __device__ __forceinline__ void hist_add(Smem& s, int b) {
   atomicAdd(&s.hist[b >> 1], 1u << ((b & 1) << 4));
 }
 
-// ---------------------------------------------------------------- E: fused tile
-// Phase A: gray over the GH x GW region at clamped coordinates (mode="nearest").  Warp w
-// walks rows w, w+8, ...; lane l covers columns l, l+32, l+64.
+// ---------------------------------------------------------------- E: fused band
+// An E task owns a band of the view: output columns [x0, x0 + xw) (xw <= TWM) and rows
+// [ya, yb).  It walks the band top to bottom in sub-steps of n <= SR output rows; shared
+// memory holds each stage's rows for the current sub-step plus the context rows the next
+// one needs (shifted down between sub-steps), so every row is computed once per band:
+//   gray    rows [Y-4, Y+4+n)   s.g  (row 0 = Y-4;  columns x0-4 .., clamped coordinates)
+//   blur    rows [Y-2, Y+2+n)   s.b  (row 0 = Y-2;  columns x0-2 ..)
+//   Sobel   rows [Y-1, Y+1+n)   s.q  (row 0 = Y-1;  columns x0-1 ..: packed |g|^2 key + bin)
+//   NMS     rows [Y,   Y+n)     decide from the keys; survivors and undecided pixels are
+//                               compacted into s.list and finished by all threads (exact
+//                               glibc hypot, map store, median histogram)
+// Hot loops run over full 128-lane column sets without per-cell bounds tests: columns past
+// the band compute harmless values that nothing reads.
+//
+// Exactness.  NMS compares glibc hypot values.  A cell's key is the top 30 bits of the IEEE
+// pattern of |g|^2 = fma(gx, gx, gy*gy); two keys more than one unit apart order the
+// magnitudes with a margin of ~2^-19 relative (the rounding of |g|^2 and the <= 1 ulp error
+// of hypot are below 2^-50).  Keys within one unit, exact-zero ties, tiny or non-finite
+// gradients (KEY_EXACT) fall back to the exact hypot of the cells involved, recomputed from
+// the blurred rows.  Surviving pixels always store the exact glibc hypot value.
+
+constexpr unsigned KEY_EXACT = 0x3fffffffu;  // key field of a cell whose order needs hypot
+
+// Packed Sobel cell: (key << 2) | direction bin.  The key is the high word of |g|^2 >> 2 when
+// 2^-960 <= |g|^2 < 2^1000 (range test on the integer high word), 0 for an exactly zero
+// gradient, KEY_EXACT otherwise (tiny, huge or NaN: order by the exact hypot).
+__device__ __forceinline__ unsigned pack_cell(double gx, double gy, int bin) {
+  const double q = fma(gx, gx, gy * gy);
+  const unsigned hi = (unsigned)__double2hiint(q);
+  unsigned key = hi >> 2;
+  if (hi - 0x03f00000u >= 0x7e700000u - 0x03f00000u)
+    key = (gx == 0.0 && gy == 0.0) ? 0u : KEY_EXACT;
+  return (key << 2) | (unsigned)bin;
+}
+
+// Gray rows [y_first, y_first + cnt) into s.g rows [r_first, r_first + cnt) (cnt <= 16).
+// Warp w handles rows w and w + NWARP; lanes handle columns lane + 32 k (k < 4) and
+// columns 128..131 in one combined pass.
+__device__ __forceinline__ void ld_rgb(const double* a, unsigned long long pol, double& r,
+                                       double& g, double& b) {
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%3], %4;\n\t"
+      "ld.global.nc.L2::cache_hint.f64 %1, [%3+8], %4;\n\t"
+      "ld.global.nc.L2::cache_hint.f64 %2, [%3+16], %4;"
+      : "=d"(r), "=d"(g), "=d"(b) : "l"(a), "l"(pol));
+}
+__device__ __forceinline__ void ld_rgb(const float* a, unsigned long long pol, double& r,
+                                       double& g, double& b) {
+  float x, y, z;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%3], %4;\n\t"
+      "ld.global.nc.L2::cache_hint.f32 %1, [%3+4], %4;\n\t"
+      "ld.global.nc.L2::cache_hint.f32 %2, [%3+8], %4;"
+      : "=f"(x), "=f"(y), "=f"(z) : "l"(a), "l"(pol));
+  r = x;
+  g = y;
+  b = z;
+}
+
 template <int CH, bool F64>
-__device__ __forceinline__ void phase_gray(const Params& p, Smem& s, int v, int y0, int x0,
-                                           unsigned long long pol) {
+__device__ void band_gray(const Params& p, Smem& s, int v, int x0, int y_first, int r_first,
+                          int cnt, unsigned long long pol) {
   using T = typename std::conditional<F64, double, float>::type;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = (int)p.H, W = (int)p.W;
   const T* img = (const T*)p.img + (long long)v * p.npx * CH;
-  int xo[3];
-  bool ok[3];
+  auto gray = [&](const T* px) -> double {
+    if (CH == 3) {
+      double rr, gg, bb;
+      ld_rgb(px, pol, rr, gg, bb);
+      double g = ((p.kgray[0] * rr) + (p.kgray[1] * gg)) + (p.kgray[2] * bb);
+      g = g > 1.0 ? 1.0 : g;  // np.clip(., 0, 1); NaN passes; the sign of a zero cannot
+      return g < 0.0 ? 0.0 : g;  // reach the output (blur sums start from +0, clip again)
+    }
+    return ld_hint(px, pol);  // a gray input is not clipped (edge_pipeline.py:134)
+  };
+  int xo[5];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const int c = lane + 32 * k;
-    ok[k] = c < GW;
-    xo[k] = clamp_i(x0 - 4 + c, 0, W - 1) * CH;
+  for (int k = 0; k < 4; ++k) xo[k] = clamp_i(x0 - 4 + lane + 32 * k, 0, W - 1) * CH;
+  xo[4] = clamp_i(x0 - 4 + 128 + (lane & 3), 0, W - 1) * CH;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = warp + NWARP * h;
+    if (r < cnt) {
+      const T* row = img + (long long)clamp_i(y_first + r, 0, H - 1) * W * CH;
+      double* dst = s.g + (r_first + r) * GWP + lane;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dst[32 * k] = gray(row + xo[k]);
+    }
   }
+  const int r = warp + NWARP * (lane >> 2);
+  if (lane < 8 && r < cnt)
+    s.g[(r_first + r) * GWP + 128 + (lane & 3)] =
+        gray(img + (long long)clamp_i(y_first + r, 0, H - 1) * W * CH + xo[4]);
+}
+
+// 5x5 blur of rows [y_first, y_first + cnt) (cnt <= 16) into s.b rows [rb_first, ...);
+// blurred s.b row R sums s.g rows R .. R+4.  Thread (c, h): blurred column c (x = x0-2+c,
+// computed at the clamped column), rows h*8 .. h*8+7, streaming the input rows top to bottom
+// so every output sums its taps in NI_Correlate's row-major order.  Rows outside the image
+// take the value of the clamped in-image row (mode="nearest" on the blurred image).
+template <bool FAST, int CH>
+__device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_first, int cnt) {
+  const int c = threadIdx.x & 127, h = threadIdx.x >> 7;
+  const int H = (int)p.H, W = (int)p.W;
+  const int r0 = h * 8;
+  if (r0 >= cnt) return;
+  const int nr = min(8, cnt - r0);
+  const int gc = clamp_i(x0 - 2 + c, 0, W - 1) - x0 + 2;  // s.g column of the leftmost tap
+  const double* gin = s.g + (rb_first + r0) * GWP + gc;
+  auto wsym = [&](int di, int dj) { return p.w6[di < 2 ? 2 - di : di - 2][dj < 2 ? 2 - dj : dj - 2]; };
+  auto finish = [&](double x) { return (CH == 3) ? (x > 1.0 ? 1.0 : x) : np_clip01_int(x); };
+  double acc[8];
 #pragma unroll
-  for (int u = warp; u < GH; u += NWARP) {
-    const T* row = img + (long long)clamp_i(y0 - 4 + u, 0, H - 1) * W * CH;
+  for (int r = 0; r < 12; ++r) {
+    double xv[5];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      if (!ok[k]) continue;
-      double g;
-      if (CH == 3) {
-        const double r = ld_hint(row + xo[k], pol), gg = ld_hint(row + xo[k] + 1, pol),
-                     bb = ld_hint(row + xo[k] + 2, pol);
-        g = np_clip01_int(((0.299 * r) + (0.587 * gg)) + (0.114 * bb));
-      } else {
-        g = ld_hint(row + xo[k], pol);
+    for (int dj = 0; dj < 5; ++dj) xv[dj] = gin[r * GWP + dj];
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      const int di = r - o;
+      if (di < 0 || di > 4) continue;
+#pragma unroll
+      for (int dj = 0; dj < 5; ++dj) {
+        const int t25 = di * 5 + dj;
+        if (FAST) {
+          const double prod = xv[dj] * wsym(di, dj);
+          acc[o] = (t25 == 0) ? prod : acc[o] + prod;
+        } else {
+          if (t25 == 0) acc[o] = 0.0;
+          if ((p.keep_mask >> t25) & 1u) acc[o] = acc[o] + xv[dj] * p.w25[t25];
+        }
       }
-      s.g[u * GW + lane + 32 * k] = g;
+    }
+  }
+  double* bout = s.b + (rb_first + r0) * BWP + c;
+  const int y0 = y_first + r0;
+  if (nr == 8) {
+#pragma unroll
+    for (int o = 0; o < 8; ++o) bout[o * BWP] = finish(acc[o]);
+  } else {
+#pragma unroll
+    for (int o = 0; o < 8; ++o)
+      if (o < nr) bout[o * BWP] = finish(acc[o]);
+  }
+  if (y0 < 0 || y0 + nr > H) {  // rare: top / bottom rows of the image
+    for (int o = 0; o < nr; ++o) {
+      const int y = y0 + o;
+      if (y >= 0 && y < H) continue;
+      const double* row = gin + (o + (clamp_i(y, 0, H - 1) - y)) * GWP;
+      double a = 0.0;
+      for (int di = 0; di < 5; ++di)
+        for (int dj = 0; dj < 5; ++dj) {
+          const int t25 = di * 5 + dj;
+          if (FAST) {
+            const double prod = row[di * GWP + dj] * wsym(di, dj);
+            a = (t25 == 0) ? prod : a + prod;
+          } else if ((p.keep_mask >> t25) & 1u) {
+            a = a + row[di * GWP + dj] * p.w25[t25];
+          }
+        }
+      bout[o * BWP] = finish(a);
     }
   }
 }
 
+__device__ __forceinline__ void sobel_at(const double* t, const double* m, const double* d,
+                                         double& gx, double& gy) {
+  // NI_Correlate tap order with the zero taps skipped; the exact x2 taps as FMAs.
+  gx = t[2] - t[0];
+  gx = fma(-2.0, m[0], gx);
+  gx = fma(2.0, m[2], gx);
+  gx = gx - d[0];
+  gx = gx + d[2];
+  gy = fma(-2.0, t[1], -t[0]);
+  gy = gy - t[2];
+  gy = gy + d[0];
+  gy = fma(2.0, d[1], gy);
+  gy = gy + d[2];
+}
+
+// Direction bin (gradient_bin) with the common case inline and its constants in the
+// kernel parameters.
+__device__ __forceinline__ int dir_bin(const Params& p, double gx, double gy) {
+  const double ax = fabs(gx), ay = fabs(gy);
+  const double d0 = fma(-p.ktan, ax, ay);   // > 0: above pi/8 from the x axis
+  const double d2 = fma(-p.ktan, ay, ax);   // > 0: below 3 pi/8
+  const double tol = p.ktol * (ax + ay);
+  if (fabs(d0) > tol && fabs(d2) > tol) {
+    const int q13 = ((__double2hiint(gx) ^ __double2hiint(gy)) >= 0) ? 1 : 3;
+    return d0 < 0.0 ? 0 : (d2 < 0.0 ? 2 : q13);
+  }
+  return gradient_bin(gx, gy);  // zero, near a boundary, or non-finite
+}
+
+// Sobel of rows [y_first, y_first + cnt) into s.q rows [rq_first, ...); s.q row R uses s.b
+// rows R .. R+2.  Thread (c, h): magnitude column c (x = x0 - 1 + c), rows h*8 .. h*8+7,
+// sliding a 3x3 window down s.b.  Cells outside the image hold 0 (edge_pipeline.py:97).
+template <bool NMS>
+__device__ void band_sobel(const Params& p, Smem& s, int x0, int y_first, int rq_first, int cnt) {
+  const int c = threadIdx.x & 127, h = threadIdx.x >> 7;
+  const int H = (int)p.H, W = (int)p.W;
+  const int r0 = h * 8;
+  if (r0 >= cnt) return;
+  const int nr = min(8, cnt - r0);
+  const int x = x0 - 1 + c;
+  const bool xin = x >= 0 && x < W;
+  const int y0 = y_first + r0;
+  const double* bin_ = s.b + (rq_first + r0) * BWP + c;
+  unsigned* qout = s.q + (rq_first + r0) * MWP + c;
+  double t[3], m[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    t[k] = bin_[k];
+    m[k] = bin_[BWP + k];
+  }
+  auto row = [&](int j, bool check) {
+    double d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = bin_[(j + 2) * BWP + k];
+    double gx, gy;
+    sobel_at(t, m, d, gx, gy);
+    unsigned cellv = pack_cell(gx, gy, NMS ? dir_bin(p, gx, gy) : 0);
+    const int y = y0 + j;
+    if (!xin || (check && (y < 0 || y >= H))) cellv = 0u;
+    qout[j * MWP] = cellv;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      t[k] = m[k];
+      m[k] = d[k];
+    }
+  };
+  if (nr == 8 && y0 >= 0 && y0 + 8 <= H) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) row(j, false);
+  } else {
+    for (int j = 0; j < nr; ++j) row(j, true);
+  }
+}
+
+// Exact glibc hypot at magnitude cell (s.q row rq, column c) of image row y (0 outside).
+__device__ __forceinline__ double mag_exact(const Params& p, const Smem& s, int x0, int y,
+                                            int rq, int c) {
+  const int x = x0 - 1 + c;
+  if (y < 0 || y >= (int)p.H || x < 0 || x >= (int)p.W) return 0.0;
+  const double* b = s.b + rq * BWP + c;
+  double gx, gy;
+  sobel_at(b, b + BWP, b + 2 * BWP, gx, gy);
+  return hypot_glibc(gx, gy);
+}
+
+// NMS decisions of output rows [y_first, y_first + cnt) (s.q row r + 1): warp w rows w and
+// w + NWARP, lane l columns l + 32 k.  Suppressed pixels store 0 here; survivors and
+// undecided pixels are appended to s.list as (r << 16) | (c << 4) | (undecided prev << 1) |
+// undecided next (warp-aggregated).
+__device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw, int y_first,
+                                int cnt, int parity) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long vbase = (long long)v * p.npx;
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int r = warp + NWARP * hh;
+    if (r >= cnt) continue;
+    const unsigned* qrow = s.q + (r + 1) * MWP + 1;  // output column c at qrow[c]
+    double* orow = p.out + vbase + (long long)(y_first + r) * p.W + x0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = lane + 32 * k;
+      const unsigned qc = qrow[c];
+      unsigned entry = 0;
+      bool need;
+      if (p.nms) {
+        const int bn = (int)(qc & 3u);
+        // prev (dy, dx): bin0 (0,-1), bin1 (-1,-1), bin2 (-1,0), bin3 (-1,+1); next = -prev
+        const int po = bn == 0 ? -1 : bn - MWP - 2;  // prev as an offset in s.q cells
+        const int kc = (int)(qc >> 2), kp = (int)(qrow[c + po] >> 2), kn = (int)(qrow[c - po] >> 2);
+        const int d1 = kc - kp, d2 = kc - kn;
+        const bool sent = kc == (int)KEY_EXACT;
+        const bool u1 = sent || kp == (int)KEY_EXACT || (d1 >= -1 && d1 <= 1 && (kc | kp) != 0);
+        const bool u2 = sent || kn == (int)KEY_EXACT || (d2 >= -1 && d2 <= 1 && (kc | kn) != 0);
+        // suppressed for sure: prev decided >= self, or next decided > self
+        const bool rej = (!u1 && d1 <= 0) || (!u2 && d2 < 0);
+        need = !rej;
+        entry = ((unsigned)r << 16) | ((unsigned)c << 4) | (u1 ? 2u : 0u) | (u2 ? 1u : 0u);
+      } else {
+        need = (qc >> 2) != 0;
+        entry = ((unsigned)r << 16) | ((unsigned)c << 4);
+      }
+      need = need && c < xw;
+      if (!need && c < xw) orow[c] = 0.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, need);
+      if (bal) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&s.list_n[parity], (unsigned)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (need) s.list[base + __popc(bal & lanemask_lt())] = entry;
+      }
+    }
+  }
+}
+
+// Finish the compacted pixels with all threads: exact magnitude, the undecided comparisons,
+// the map store (L2 evict_last) and the median histogram.
+__device__ void band_nms_finish(const Params& p, Smem& s, int v, int x0, int y_first, int parity,
+                                unsigned long long pol_mid) {
+  const unsigned n = s.list_n[parity];
+  const long long vbase = (long long)v * p.npx;
+  for (unsigned i = threadIdx.x; i < n; i += NT) {
+    const unsigned e = s.list[i];
+    const int r = (int)(e >> 16), c = (int)((e >> 4) & 0xfffu);
+    const int y = y_first + r;
+    const double m = mag_exact(p, s, x0, y, r + 1, c + 1);
+    bool keep = true;
+    if (e & 3u) {
+      const int bn = (int)(s.q[(r + 1) * MWP + 1 + c] & 3u);
+      const int dy = bn == 0 ? 0 : -1, dx = bn == 0 ? -1 : bn - 2;
+      if (e & 2u) keep = m > mag_exact(p, s, x0, y + dy, r + 1 + dy, c + 1 + dx);
+      if (keep && (e & 1u)) keep = m >= mag_exact(p, s, x0, y - dy, r + 1 - dy, c + 1 - dx);
+    }
+    const double outv = keep ? m : 0.0;
+    st_hint(p.out + vbase + (long long)y * p.W + x0 + c, outv, pol_mid);
+    if (p.median && outv > 0.0) hist_add(s, hist_bin(outv));
+  }
+}
+
+template <int CH, bool F64>
+__device__ void prefetch_rows(const Params& p, int v, int x0, int xw, int y_lo, int y_hi,
+                              unsigned long long pol);
+
 template <int CH, bool F64>
 __device__ void claim_next(const Params& p, Smem& s, unsigned long long pol_in);
 
+// Copy rows [from, from + n) (n <= NWARP) of a shared array of pitch P to rows [0, n):
+// warp wbase + r copies row r, lanes the columns.
+template <typename E, int P>
+__device__ __forceinline__ void shift_rows(E* a, int from, int n, int wbase = 0) {
+  const int lane = threadIdx.x & 31, r = (int)(threadIdx.x >> 5) - wbase;
+  if (r >= 0 && r < n) {
+    const E* src = a + (from + r) * P;
+    E* dst = a + r * P;
+#pragma unroll
+    for (int c = lane; c < P; c += 32) dst[c] = src[c];
+  }
+}
+
 template <bool FAST, int CH, bool F64>
-__device__ void run_tile(const Params& p, Smem& s, int v, int t, unsigned long long pol_in,
+__device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long long pol_in,
                          unsigned long long pol_mid) {
-  const int tid = threadIdx.x;
   const int H = (int)p.H, W = (int)p.W;
-  const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
-  const int y0 = ty * TH, x0 = tx * TW;
-  const long long vbase = (long long)v * p.npx;
-
-  phase_gray<CH, F64>(p, s, v, y0, x0, pol_in);
+  const int cb = t % p.ncols, rb = t / p.ncols;
+  const int x0 = cb * p.tw, xw = min(p.tw, W - x0);
+  const int ya = rb * p.band_h, yb = min(ya + p.band_h, H);
+  // prologue: gray rows [ya-4, ya+4) -> s.g rows 0..7; blurred [ya-2, ya+2) -> s.b rows 0..3;
+  // Sobel rows [ya-1, ya+1) -> s.q rows 0..1
+  if (threadIdx.x == 0) s.list_n[0] = 0;
+  band_gray<CH, F64>(p, s, v, x0, ya - 4, 0, 8, pol_in);
   __syncthreads();
-
-  // Phase B: 5x5 blur in vertical strips of SB outputs per thread.  Input rows stream top
-  // to bottom, so every output accumulates its taps in NI_Correlate's row-major order.  With
-  // dihedrally symmetric weights (FAST) the products of rows r-o and r-(4-o) are shared.
-  // Each sum starts from its first product: identical to 0.0 + p except for the sign of an
-  // all-zero sum, which the clip maps to +0 either way.
-  {
-    const int c = tid % BW, u0 = (tid / BW) * SB;
-    double acc[SB];
-#pragma unroll
-    for (int r = 0; r < SB + 4; ++r) {
-      double xv[5];
-#pragma unroll
-      for (int dj = 0; dj < 5; ++dj) xv[dj] = s.g[(u0 + r) * GW + c + dj];
-#pragma unroll
-      for (int o = 0; o < SB; ++o) {
-        const int di = r - o;
-        if (di < 0 || di > 4) continue;
-#pragma unroll
-        for (int dj = 0; dj < 5; ++dj) {
-          const int t25 = di * 5 + dj;
-          if (FAST) {
-            const double prod = xv[dj] * p.w6[di < 2 ? 2 - di : di - 2][dj < 2 ? 2 - dj : dj - 2];
-            acc[o] = (t25 == 0) ? prod : acc[o] + prod;
-          } else {
-            if (t25 == 0) acc[o] = 0.0;
-            if ((p.keep_mask >> t25) & 1u) acc[o] = acc[o] + xv[dj] * p.w25[t25];
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 0; o < SB; ++o) {
-      // RGB input: gray in [0, 1] and positive weights keep the sum >= +0, so only the
-      // upper clip can bite (NaN passes through as in np.clip).  Gray input: full clip.
-      const double x = acc[o];
-      s.b[(u0 + o) * BW + c] = (CH == 3) ? (x > 1.0 ? 1.0 : x) : np_clip01_int(x);
-    }
-  }
+  band_blur<FAST, CH>(p, s, x0, ya - 2, 0, 4);
   __syncthreads();
-  // Border tiles: out-of-image blurred cells take the value of the clamped in-image cell.
-  if (y0 < 2 || x0 < 2 || y0 + TH + 2 > H || x0 + TW + 2 > W) {
-    constexpr int FIX = BH * BW / NT;
-    static_assert(BH * BW % NT == 0, "fix-up covers the blurred region exactly");
-    double val[FIX];
-    bool fix[FIX];
-#pragma unroll
-    for (int k = 0; k < FIX; ++k) {
-      const int i = tid + k * NT, u = i / BW, c = i - u * BW;
-      const int y = y0 - 2 + u, x = x0 - 2 + c;
-      const int cy = clamp_i(y, 0, H - 1), cx = clamp_i(x, 0, W - 1);
-      fix[k] = (cy != y) || (cx != x);
-      val[k] = fix[k] ? s.b[(cy - (y0 - 2)) * BW + (cx - (x0 - 2))] : 0.0;
+  if (p.nms) band_sobel<true>(p, s, x0, ya - 1, 0, 2);
+  else band_sobel<false>(p, s, x0, ya - 1, 0, 2);
+  int parity = 0;
+  for (int Y = ya; Y < yb; Y += SR) {
+    const int n = min(SR, yb - Y);
+    const bool more = Y + SR < yb;
+    if (threadIdx.x < 32) {  // warp 0: L2 prefetch of the next sub-step's input rows, or
+                             // (last sub-step) the claim of the next task
+      if (more) prefetch_rows<CH, F64>(p, v, x0, xw, Y + SR + 4, min(Y + 2 * SR, yb) + 4, pol_in);
+      else claim_next<CH, F64>(p, s, pol_in);
     }
+    if (threadIdx.x == 32) s.list_n[parity ^ 1] = 0;  // the next sub-step's list
+    // s.g rows 0..7 hold gray [Y-4, Y+4); new gray rows [Y+4, Y+4+n) -> rows 8 ..
+    band_gray<CH, F64>(p, s, v, x0, Y + 4, 8, n, pol_in);
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < FIX; ++k)
-      if (fix[k]) s.b[tid + k * NT] = val[k];
+    // s.b rows 0..3 hold blurred [Y-2, Y+2); new rows [Y+2, Y+2+n) -> rows 4 ..
+    band_blur<FAST, CH>(p, s, x0, Y + 2, 4, n);
     __syncthreads();
-  }
-
-  // Phase C: Sobel (NI_Correlate tap order; the zero taps are skipped as scipy does; the
-  // exact x2 taps as FMAs), glibc hypot, direction bin of the output pixels.  Thread (c, k)
-  // owns column c, rows 9k..9k+8 of the magnitude region and slides a 3x3 window down.
-  {
-    constexpr int SS = 9, NSTRIP = (MH + SS - 1) / SS;
-    static_assert(MW * NSTRIP <= NT, "one strip per thread");
-    const int c = tid % MW, k = tid / MW;
-    if (k < NSTRIP) {
-      const int x = x0 - 1 + c;
-      const bool xin = x >= 0 && x < W;
-      const double* col = &s.b[(k * SS) * BW + c];
-      double t0 = col[0], t1 = col[1], t2 = col[2];
-      double m0 = col[BW], m2 = col[BW + 2], m1 = col[BW + 1];
-#pragma unroll
-      for (int j = 0; j < SS; ++j) {
-        const int u = k * SS + j;
-        if (u >= MH) break;
-        const double* nb = col + (j + 2) * BW;
-        const double d0 = nb[0], d1 = nb[1], d2 = nb[2];
-        const int y = y0 - 1 + u;
-        double m = 0.0;  // out-of-image neighbours count as 0 for NMS (edge_pipeline.py:97)
-        if (xin && y >= 0 && y < H) {
-          double gx = t2 - t0;                // (0 + -b00) + b02
-          gx = fma(-2.0, m0, gx);
-          gx = fma(2.0, m2, gx);
-          gx = gx - d0;
-          gx = gx + d2;
-          double gy = fma(-2.0, t1, -t0);     // (0 + -b00) + -2 b01
-          gy = gy - t2;
-          gy = gy + d0;
-          gy = fma(2.0, d1, gy);
-          gy = gy + d2;
-          m = (CH == 3) ? hypot_glibc_fast_bounded(gx, gy) : hypot_glibc_fast(gx, gy);
-          if (p.nms && u >= 1 && u <= TH && c >= 1 && c <= TW)
-            s.bin[(u - 1) * TW + (c - 1)] = (uint8_t)gradient_bin(gx, gy);
-        }
-        s.g[u * MW + c] = m;  // gray is dead after phase B
-        t0 = m0; t1 = m1; t2 = m2;
-        m0 = d0; m1 = d1; m2 = d2;
-      }
-    }
-  }
-  __syncthreads();
-
-  // Phase D: NMS (keep iff m > prev and m >= next; magnitudes are >= +0 or NaN, so the
-  // comparisons run on the bit patterns), store with L2 evict_last, histogram survivors.
-  if (tid == 0) claim_next<CH, F64>(p, s, pol_in);
-  {
-    const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-    for (int a = warp; a < TH; a += NWARP) {
-      const int y = y0 + a;
-      if (y >= H) break;
-      double* orow = p.out + vbase + (long long)y * W + x0;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int c = lane + 32 * k;
-        if (c >= TW || x0 + c >= W) continue;
-        const double* mp = &s.g[(a + 1) * MW + (c + 1)];
-        const double m = *mp;
-        double outv = m;
-        if (p.nms) {
-          const int bn = s.bin[a * TW + c];
-          const int po = bn == 0 ? -1 : (bn == 1 ? -MW - 1 : (bn == 2 ? -MW : -MW + 1));
-          const long long mb = __double_as_longlong(m);
-          const bool keep = (mb <= 0x7ff0000000000000LL) &&
-                            (mb > __double_as_longlong(mp[po])) &&
-                            (mb >= __double_as_longlong(mp[-po]));
-          outv = keep ? m : 0.0;
-        }
-        st_hint(orow + c, outv, pol_mid);
-        if (p.median && outv > 0.0) hist_add(s, hist_bin(outv));
-      }
+    // s.q rows 0..1 hold Sobel [Y-1, Y+1); new rows [Y+1, Y+1+n) -> rows 2 ..; meanwhile keep
+    // gray rows [Y+n-4, Y+n+4) for the next sub-step
+    if (p.nms) band_sobel<true>(p, s, x0, Y + 1, 2, n);
+    else band_sobel<false>(p, s, x0, Y + 1, 2, n);
+    if (more) shift_rows<double, GWP>(s.g, n, 8);
+    __syncthreads();
+    band_nms_decide(p, s, v, x0, xw, Y, n, parity);
+    __syncthreads();
+    band_nms_finish(p, s, v, x0, Y, parity, pol_mid);
+    parity ^= 1;
+    __syncthreads();
+    if (more) {  // context rows for the next sub-step (read by the next blur / NMS)
+      shift_rows<double, BWP>(s.b, n, 4);
+      shift_rows<unsigned, MWP>(s.q, n, 2, 4);
     }
   }
 }
@@ -490,7 +701,7 @@ __device__ __forceinline__ int sub_bin(unsigned long long bits) {
 // not limited by register-held loads.  Unaligned views fall back to plain loads.
 constexpr int PIECE = 2048;                     // doubles per piece (16 KB)
 constexpr int STAGE = 256;                      // staged candidates per list in a C task
-static_assert(2 * PIECE + 2 * STAGE <= GH * GW + BH * BW, "stream buffers fit in g + b");
+static_assert(2 * PIECE + 2 * STAGE <= GR * GWP + BR * BWP, "stream buffers fit in g + b");
 
 // g and b are contiguous doubles at the start of Smem: one arena for C/A/select scratch.
 __device__ __forceinline__ double* arena(Smem& s) { return reinterpret_cast<double*>(&s); }
@@ -798,7 +1009,7 @@ __device__ void run_apply(const Params& p, Smem& s, int v, int c, unsigned long 
 // ------------------------------------------------------------- scheduler
 // Thread 0 claims the next task, in priority order: an A chunk of the oldest view whose
 // median is published, a C chunk of the oldest view whose bins are published (and whose
-// candidate ring slot is free), else the next E tile if it is at most AHEAD views past the
+// candidate ring slot is free), else the next E band if it is at most `ahead` views past the
 // A front (bounding the L2-resident thinned maps).  A/C work is claimed only when ready, so
 // no task ever waits; TASK_NONE means "nothing ready right now".
 enum TaskKind { TASK_END = 0, TASK_E = 1, TASK_C = 2, TASK_A = 3, TASK_NONE = 4 };
@@ -848,7 +1059,7 @@ __device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
   unsigned long long* e_next = (unsigned long long*)&sched[4];
   unsigned long long t = ld_acquire64(e_next);
   // throttle (racy by design: concurrent claimers may overshoot by about one view)
-  if (t < total_e && !(p.median && t / p.TE >= ld_acquire(&sched[2]) + AHEAD)) {
+  if (t < total_e && !(p.median && t / p.TE >= ld_acquire(&sched[2]) + (unsigned)p.ahead)) {
     t = atomicAdd(e_next, 1ull);  // an atomicAdd never retries, unlike a CAS claim
     if (t < total_e) {
       const unsigned v = (unsigned)(t / p.TE);
@@ -863,18 +1074,19 @@ __device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
   kind = ld_acquire(&sched[2]) >= B ? TASK_END : TASK_NONE;
 }
 
-// L2 prefetch of an E task's input rows, one bulk prefetch per row, issued by thread 0 one
-// task ahead with the input's evict_first policy.
+// L2 prefetch of input rows [y_lo, y_hi) (clamped) of a band: one bulk prefetch per row,
+// the rows spread over the lanes of the calling warp, with the input's evict_first policy.
 template <int CH, bool F64>
-__device__ void prefetch_tile(const Params& p, int v, int t, unsigned long long pol) {
+__device__ void prefetch_rows(const Params& p, int v, int x0, int xw, int y_lo, int y_hi,
+                              unsigned long long pol) {
   using T = typename std::conditional<F64, double, float>::type;
-  const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
   const int H = (int)p.H, W = (int)p.W;
-  const int xl = clamp_i(tx * TW - 4, 0, W - 1), xh = clamp_i(tx * TW + TW + 4, 1, W);
+  const int xl = clamp_i(x0 - 4, 0, W - 1), xh = clamp_i(x0 + xw + 4, 1, W);
   const char* base = (const char*)p.img;
   const unsigned long long total = ((unsigned long long)p.B * p.npx * CH * sizeof(T)) & ~15ull;
-  const int ylo = clamp_i(ty * TH - 4, 0, H - 1), yhi = clamp_i(ty * TH + TH + 4, 1, H);
-  for (int y = ylo; y < yhi; ++y) {
+  y_lo = clamp_i(y_lo, 0, H);
+  y_hi = clamp_i(y_hi, 0, H);
+  for (int y = y_lo + (int)(threadIdx.x & 31); y < y_hi; y += 32) {
     const unsigned long long row = (unsigned long long)v * p.npx + (unsigned long long)y * W;
     unsigned long long a = ((row + xl) * CH * sizeof(T)) & ~15ull;
     unsigned long long e = ((row + xh) * CH * sizeof(T) + 15) & ~15ull;
@@ -886,19 +1098,32 @@ __device__ void prefetch_tile(const Params& p, int v, int t, unsigned long long 
   }
 }
 
+template <int CH, bool F64>
+__device__ void prefetch_band_start(const Params& p, int v, int t, unsigned long long pol) {
+  const int cb = t % p.ncols, rb = t / p.ncols;
+  const int x0 = cb * p.tw, xw = min(p.tw, (int)p.W - x0);
+  const int ya = rb * p.band_h;
+  prefetch_rows<CH, F64>(p, v, x0, xw, ya - 4, ya + SR + 4, pol);
+}
+
 // Thread 0: claim the next task into s.task_* and warm L2 with its input rows.
 template <int CH, bool F64>
 __device__ void claim_next(const Params& p, Smem& s, unsigned long long pol_in) {
-  int nk = 0, nv = 0, ni = 0;
-  claim_task(p, nk, nv, ni);
-  s.task_kind = nk;
-  s.task_view = nv;
-  s.task_idx = ni;
-  if (nk == TASK_E && p.mode == MODE_FUSED) prefetch_tile<CH, F64>(p, nv, ni, pol_in);
+  // called by a whole warp: lane 0 claims, the warp prefetches the first rows of a band
+  if ((threadIdx.x & 31) == 0) {
+    int nk = 0, nv = 0, ni = 0;
+    claim_task(p, nk, nv, ni);
+    s.task_kind = nk;
+    s.task_view = nv;
+    s.task_idx = ni;
+  }
+  __syncwarp();
+  if (s.task_kind == TASK_E && p.mode == MODE_FUSED)
+    prefetch_band_start<CH, F64>(p, s.task_view, s.task_idx, pol_in);
 }
 
 template <bool FAST, int CH, bool F64>
-__global__ void __launch_bounds__(NT, 4) edge_persistent_kernel(Params p) {
+__global__ void __launch_bounds__(NT, 3) edge_persistent_kernel(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   for (int i = threadIdx.x; i < NB / 2; i += NT) s.hist[i] = 0;
@@ -919,12 +1144,12 @@ __global__ void __launch_bounds__(NT, 4) edge_persistent_kernel(Params p) {
     __syncthreads();
     if (kind == TASK_END) break;
     const unsigned long long t_start = trace ? gtimer() : 0ull;
-    // Claim the next task while this one runs: short tasks claim now; a fused tile claims at
-    // the start of its NMS phase, so ready C/A work is not held behind a whole tile.
+    // Claim the next task while this one runs: short tasks claim now; a fused band claims at
+    // the start of its last sub-step, so ready C/A work is not held behind a whole band.
     const bool late_claim = kind == TASK_E && p.mode == MODE_FUSED;
-    if (threadIdx.x == 0 && !late_claim) claim_next<CH, F64>(p, s, pol_in);
+    if (threadIdx.x < 32 && !late_claim) claim_next<CH, F64>(p, s, pol_in);
     if (kind == TASK_E) {
-      if (p.mode == MODE_FUSED) run_tile<FAST, CH, F64>(p, s, v, idx, pol_in, pol_mid);
+      if (p.mode == MODE_FUSED) run_band<FAST, CH, F64>(p, s, v, idx, pol_in, pol_mid);
       else run_hist_chunk(p, s, v, idx);
       if (p.median) {
         flush_hist(p, s, v);
@@ -1026,10 +1251,19 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   p.cand = (double*)(w + L.cand);
   p.slots = (double*)(w + L.slots);
   IGS_CUDA_TRY(cudaMemsetAsync(w, 0, L.zero_bytes, stream));  // sched, ctl, hist, hist2
+  p.kgray[0] = 0.299;
+  p.kgray[1] = 0.587;
+  p.kgray[2] = 0.114;
+  p.ktan = 0.41421356237309503;
+  p.ktol = 1e-12;
   if (p.mode == MODE_FUSED) {
-    p.tiles_x = (int)((p.W + TW - 1) / TW);
-    p.tiles_y = (int)((p.H + TH - 1) / TH);
-    p.TE = p.tiles_x * p.tiles_y;
+    p.ncols = (int)((p.W + TWM - 1) / TWM);
+    p.tw = (int)((p.W + p.ncols - 1) / p.ncols);
+    int bh = BAND_H;  // tuning override (IGS_BAND_H, clamped to [SR, BAND_H])
+    if (const char* e = getenv("IGS_BAND_H")) bh = atoi(e) < SR ? SR : (atoi(e) > BAND_H ? BAND_H : atoi(e));
+    const int nbands = (int)((p.H + bh - 1) / bh);
+    p.band_h = (int)((p.H + nbands - 1) / nbands);
+    p.TE = p.ncols * nbands;
   } else {
     p.TE = (int)((p.npx + CHUNK - 1) / CHUNK);
   }
@@ -1045,6 +1279,12 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   else fast ? pick<true, 1, false>(fn, bps) : pick<false, 1, false>(fn, bps);
   if (bps <= 0) return IGS_ERR_CUDA;
   long long grid = (long long)bps * sm_count();
+  // enough E work in flight to occupy the grid, bounded by the candidate ring
+  {
+    long long a = (grid + p.TE - 1) / p.TE + 1;
+    if (const char* e = getenv("IGS_AHEAD")) a = atoi(e);
+    p.ahead = (int)(a < 2 ? 2 : (a > RING - 2 ? RING - 2 : a));
+  }
   const long long total_tasks = (long long)(p.TE + p.TC + p.TA) * p.B;
   if (grid > total_tasks) grid = total_tasks;
   if (grid < 1) grid = 1;

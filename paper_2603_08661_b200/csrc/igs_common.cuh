@@ -219,6 +219,23 @@ __device__ __forceinline__ int gradient_bin(double gx, double gy) {
   return ((gx > 0.0) == (gy > 0.0)) ? 1 : 3;
 }
 
+// gradient_bin with the common case first: no zero tests (an axis-aligned gradient is decided
+// by the same margin test), the quadrant from the sign bits.  Exactly zero, near-boundary and
+// non-finite gradients take gradient_bin.
+__device__ __forceinline__ int gradient_bin_fast(double gx, double gy) {
+  const double kTan = 0.41421356237309503;  // tan(pi/8)
+  const double ax = fabs(gx), ay = fabs(gy);
+  const double d0 = fma(-kTan, ax, ay);
+  const double d2 = fma(-kTan, ay, ax);
+  const double tol = 1e-12 * (ax + ay);
+  if (fabs(d0) > tol && fabs(d2) > tol) {
+    if (d0 < 0.0) return 0;
+    if (d2 < 0.0) return 2;
+    return ((__double2hiint(gx) ^ __double2hiint(gy)) >= 0) ? 1 : 3;
+  }
+  return gradient_bin(gx, gy);
+}
+
 // ---- block helpers ----------------------------------------------------------
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
