@@ -45,7 +45,8 @@ constexpr int NT = 256;                      // threads per block
 constexpr int NWARP = NT / 32;
 constexpr int SR = 16;                       // output rows per band sub-step
 constexpr int TWM = 124;                     // max output columns per band
-constexpr int BAND_H = 128;                  // max rows per band
+constexpr int BAND_H = 128;                  // max rows per band (tuning override)
+constexpr int BAND_H_DEFAULT = 64;           // rows per band
 constexpr int GWP = TWM + 8, BWP = 128, MWP = 128;  // row pitches (cells); the blur /
                                                     // Sobel lanes cover 128 columns
 constexpr int GR = SR + 8, BR = SR + 4, QR = SR + 2;        // rows per sub-step + context
@@ -61,7 +62,7 @@ constexpr int SUB_SHIFT = 34;                // level-2 bin = bits 45..34 inside
 constexpr int SLOTS = 8;                     // candidates kept per level-2 bin
 constexpr int NB2 = 4096;                    // level-2 histogram: bits 47..36 inside a bin
 constexpr int CHUNK = 16384;                 // pixels per collect/apply task (< 65536)
-constexpr int RING = 12;                     // candidate buffers / level-2 histograms in flight
+constexpr int RING = 16;                     // candidate buffers / level-2 histograms in flight
 constexpr int SEL_CAP = GR * GWP + BR * BWP;  // doubles of smem the select may use
 
 enum Mode { MODE_FUSED = 0, MODE_MEDIAN_ONLY = 1 };
@@ -78,7 +79,9 @@ struct ViewCtl {            // per-view control block, zeroed before launch
   double denom;             // 2 * median
   double median;
   unsigned c_claim, a_claim;// C / A chunks handed out
-  unsigned pad[12];
+  unsigned nsurv;           // fused mode: positive survivors appended by the E tasks
+  unsigned tca;             // C / A tasks of this view (fused: survivor chunks)
+  unsigned pad[10];
 };
 static_assert(sizeof(ViewCtl) == 128, "one ViewCtl per 128-byte line");
 
@@ -109,8 +112,19 @@ struct Params {
   unsigned* hist;           // (B, NB)
   unsigned* hist2;          // (RING, 2, NB2)
   double* slots;            // (RING, 2, NB2, SLOTS) candidates bucketed by level-2 bin
-  double* cand;             // (RING, npx)
+  double* cand;             // (RING, slot): fused mode: survivor values [0, npx), survivor
+                            // indices (u32) [npx, 1.5 npx), candidate lists [2 npx, 3 npx);
+                            // median-only mode: candidate lists [0, npx)
+  long long slot;           // doubles per ring slot
 };
+
+__device__ __forceinline__ double* ring_slot(const Params& p, int v) {
+  return p.cand + (long long)(v % RING) * p.slot;
+}
+// the collect pass's two candidate lists: list 1 grows up from here, list 2 down from +npx-1
+__device__ __forceinline__ double* cand_lists(const Params& p, int v) {
+  return ring_slot(p, v) + (p.mode == MODE_FUSED ? 2 * p.npx : 0);
+}
 
 struct __align__(16) Smem {
   double g[GR * GWP];       // gray rows of a band sub-step; C/A stream buffers, select scratch
@@ -507,21 +521,45 @@ __device__ void band_nms_finish(const Params& p, Smem& s, int v, int x0, int y_f
                                 unsigned long long pol_mid) {
   const unsigned n = s.list_n[parity];
   const long long vbase = (long long)v * p.npx;
-  for (unsigned i = threadIdx.x; i < n; i += NT) {
-    const unsigned e = s.list[i];
-    const int r = (int)(e >> 16), c = (int)((e >> 4) & 0xfffu);
-    const int y = y_first + r;
-    const double m = mag_exact(p, s, x0, y, r + 1, c + 1);
-    bool keep = true;
-    if (e & 3u) {
-      const int bn = (int)(s.q[(r + 1) * MWP + 1 + c] & 3u);
-      const int dy = bn == 0 ? 0 : -1, dx = bn == 0 ? -1 : bn - 2;
-      if (e & 2u) keep = m > mag_exact(p, s, x0, y + dy, r + 1 + dy, c + 1 + dx);
-      if (keep && (e & 1u)) keep = m >= mag_exact(p, s, x0, y - dy, r + 1 - dy, c + 1 - dx);
+  double* sval = ring_slot(p, v);
+  unsigned* sidx = reinterpret_cast<unsigned*>(sval + p.npx);
+  for (unsigned base = 0; base < n; base += NT) {  // warp-uniform trip count
+    const unsigned i = base + threadIdx.x;
+    bool surv = false;
+    double outv = 0.0;
+    unsigned pix = 0;
+    if (i < n) {
+      const unsigned e = s.list[i];
+      const int r = (int)(e >> 16), c = (int)((e >> 4) & 0xfffu);
+      const int y = y_first + r;
+      const double m = mag_exact(p, s, x0, y, r + 1, c + 1);
+      bool keep = true;
+      if (e & 3u) {
+        const int bn = (int)(s.q[(r + 1) * MWP + 1 + c] & 3u);
+        const int dy = bn == 0 ? 0 : -1, dx = bn == 0 ? -1 : bn - 2;
+        if (e & 2u) keep = m > mag_exact(p, s, x0, y + dy, r + 1 + dy, c + 1 + dx);
+        if (keep && (e & 1u)) keep = m >= mag_exact(p, s, x0, y - dy, r + 1 - dy, c + 1 - dx);
+      }
+      outv = keep ? m : 0.0;
+      pix = (unsigned)(y * p.W + x0 + c);
+      // with the median: a positive survivor goes to the view's survivor list (the apply
+      // pass writes its normalised value); everything else is final here (0 / NaN stay)
+      surv = p.median && outv > 0.0;
+      if (surv) hist_add(s, hist_bin(outv));
+      else st_hint(p.out + vbase + pix, outv, pol_mid);
     }
-    const double outv = keep ? m : 0.0;
-    st_hint(p.out + vbase + (long long)y * p.W + x0 + c, outv, pol_mid);
-    if (p.median && outv > 0.0) hist_add(s, hist_bin(outv));
+    if (p.median) {
+      const unsigned bal = __ballot_sync(0xffffffffu, surv);
+      if (bal) {
+        unsigned at = 0;
+        if ((threadIdx.x & 31) == 0) at = atomicAdd(&p.ctl[v].nsurv, (unsigned)__popc(bal));
+        at = __shfl_sync(0xffffffffu, at, 0) + __popc(bal & lanemask_lt());
+        if (surv) {
+          sval[at] = outv;
+          sidx[at] = pix;
+        }
+      }
+    }
   }
 }
 
@@ -683,6 +721,8 @@ __device__ void find_median_bins(const Params& p, Smem& s, int v) {
       ctl.r2 = r2;
     }
   }
+  if (threadIdx.x == 0)  // fused: C and A tasks walk the survivor list (total entries)
+    ctl.tca = p.mode == MODE_FUSED ? (unsigned)((total + CHUNK - 1) / CHUNK) : (unsigned)p.TC;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -779,16 +819,18 @@ __device__ void run_collect(const Params& p, Smem& s, int v, int c) {
   const int npos = s.ivals[0], b1 = s.scratch[0], b2 = s.scratch[1];
   __syncthreads();
   if (!npos) return;
-  const double* src = (p.mode == MODE_FUSED) ? p.out + (long long)v * p.npx
-                                             : (const double*)p.img + (long long)v * p.npx;
+  // fused: a chunk of the view's survivor list; median-only: a chunk of the input array
+  const bool fused = p.mode == MODE_FUSED;
+  const double* src = fused ? ring_slot(p, v) : (const double*)p.img + (long long)v * p.npx;
+  const long long nsrc = fused ? (long long)__ldcg(&ctl.nsurv) : p.npx;
   const int slot = v % RING;
-  double* cand = p.cand + (long long)slot * p.npx;
+  double* cand = cand_lists(p, v);
   double* cand2 = cand + p.npx - 1;
   unsigned* h2a = p.hist2 + (long long)slot * 2 * NB2;
   unsigned* h2b = h2a + NB2;
   double* sla = p.slots + (long long)slot * 2 * NB2 * SLOTS;
   double* slb = sla + NB2 * SLOTS;
-  const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
+  const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, nsrc);
   stream_chunk(s, src, lo, hi, [&](long long, double x) {
     if (!(x > 0.0)) return;
     const int hb = hist_bin(x);
@@ -948,7 +990,7 @@ __device__ double resolve(Smem& s, const Want& w, const double* slots) {
 __device__ void run_select(const Params& p, Smem& s, int v) {
   ViewCtl& ctl = p.ctl[v];
   const int slot = v % RING;
-  const double* cand = p.cand + (long long)slot * p.npx;
+  const double* cand = cand_lists(p, v);
   const unsigned* h2a = p.hist2 + (long long)slot * 2 * NB2;
   const unsigned* h2b = h2a + NB2;
   const double* sla = p.slots + (long long)slot * 2 * NB2 * SLOTS;
@@ -997,9 +1039,32 @@ __device__ void run_apply(const Params& p, Smem& s, int v, int c, unsigned long 
   const double denom = __ldcg(&ctl.denom);
   const double rd = __drcp_rn(denom);
   const bool plain = isfinite(denom) && denom > 0x1p-1000 && denom < 0x1p+1000;
-  const double* src = (p.mode == MODE_FUSED) ? p.out + (long long)v * p.npx
-                                             : (const double*)p.img + (long long)v * p.npx;
   double* dst = p.out + (long long)v * p.npx;
+  if (p.mode == MODE_FUSED) {
+    // survivors only: every other pixel of the thinned map is 0 (0 / 2m = 0) or NaN already
+    const double* sval = ring_slot(p, v);
+    const unsigned* sidx = reinterpret_cast<const unsigned*>(sval + p.npx);
+    const long long n = (long long)__ldcg(&ctl.nsurv);
+    const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, n);
+    constexpr int U = 4;
+    for (long long b = lo; b < hi; b += U * NT) {
+      double x[U];
+      unsigned ix[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long k = b + u * NT + threadIdx.x;
+        if (k < hi) {
+          x[u] = __ldcg(sval + k);
+          ix[u] = __ldcg(sidx + k);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (b + u * NT + threadIdx.x < hi) st_hint(dst + ix[u], normalise(x[u], denom, rd, plain), pol_out);
+    }
+    return;
+  }
+  const double* src = (const double*)p.img + (long long)v * p.npx;
   const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
   stream_chunk(s, src, lo, hi, [&](long long i, double x) {
     st_hint(dst + i, normalise(x, denom, rd, plain), pol_out);
@@ -1037,7 +1102,7 @@ __device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
       const unsigned v = ld_acquire(&sched[2]);
       if (v >= B || !ld_acquire(&p.ctl[v].select_done)) break;
       const unsigned c = atomicAdd(&p.ctl[v].a_claim, 1u);
-      if (c < (unsigned)p.TA) {
+      if (c < __ldcg(&p.ctl[v].tca)) {
         kind = TASK_A; view = (int)v; idx = (int)c;
         return;
       }
@@ -1048,7 +1113,7 @@ __device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
       if (v >= B || !ld_acquire(&p.ctl[v].binfound)) break;
       if (v >= (unsigned)RING && !ld_acquire(&p.ctl[v - RING].select_done)) break;
       const unsigned c = atomicAdd(&p.ctl[v].c_claim, 1u);
-      if (c < (unsigned)p.TC) {
+      if (c < __ldcg(&p.ctl[v].tca)) {
         kind = TASK_C; view = (int)v; idx = (int)c;
         return;
       }
@@ -1168,7 +1233,7 @@ __global__ void __launch_bounds__(NT, 3) edge_persistent_kernel(Params p) {
       if (threadIdx.x == 0) {
         __threadfence();
         s.flag = __ldcg(&p.ctl[v].npos) &&
-                 (atomicAdd(&p.ctl[v].collect_done, 1u) == (unsigned)p.TC - 1);
+                 (atomicAdd(&p.ctl[v].collect_done, 1u) == __ldcg(&p.ctl[v].tca) - 1);
         if (s.flag) __threadfence();
       }
       __syncthreads();
@@ -1210,7 +1275,7 @@ Layout layout(long long B, long long npx, bool median) {
   L.slots = off;
   off = align_up(off + sizeof(double) * 2 * NB2 * SLOTS * (size_t)RING, 256);
   L.cand = off;
-  if (median) off = align_up(off + sizeof(double) * (size_t)npx * (size_t)(B < RING ? B : RING), 256);
+  if (median) off = align_up(off + sizeof(double) * 3 * (size_t)npx * (size_t)(B < RING ? B : RING), 256);
   L.total = off;
   return L;
 }
@@ -1249,6 +1314,7 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   p.hist = (unsigned*)(w + L.hist);
   p.hist2 = (unsigned*)(w + L.hist2);
   p.cand = (double*)(w + L.cand);
+  p.slot = 3 * p.npx;
   p.slots = (double*)(w + L.slots);
   IGS_CUDA_TRY(cudaMemsetAsync(w, 0, L.zero_bytes, stream));  // sched, ctl, hist, hist2
   p.kgray[0] = 0.299;
@@ -1259,7 +1325,7 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   if (p.mode == MODE_FUSED) {
     p.ncols = (int)((p.W + TWM - 1) / TWM);
     p.tw = (int)((p.W + p.ncols - 1) / p.ncols);
-    int bh = BAND_H;  // tuning override (IGS_BAND_H, clamped to [SR, BAND_H])
+    int bh = BAND_H_DEFAULT;  // tuning override (IGS_BAND_H, clamped to [SR, BAND_H])
     if (const char* e = getenv("IGS_BAND_H")) bh = atoi(e) < SR ? SR : (atoi(e) > BAND_H ? BAND_H : atoi(e));
     const int nbands = (int)((p.H + bh - 1) / bh);
     p.band_h = (int)((p.H + nbands - 1) / nbands);
@@ -1281,7 +1347,9 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   long long grid = (long long)bps * sm_count();
   // enough E work in flight to occupy the grid, bounded by the candidate ring
   {
-    long long a = (grid + p.TE - 1) / p.TE + 1;
+    // as many views in flight as the candidate ring allows: the collect / select / apply
+    // latency of a view is hidden behind later views' E work (measured: more is faster)
+    long long a = RING - 2;
     if (const char* e = getenv("IGS_AHEAD")) a = atoi(e);
     p.ahead = (int)(a < 2 ? 2 : (a > RING - 2 ? RING - 2 : a));
   }
