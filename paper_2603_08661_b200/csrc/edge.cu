@@ -61,7 +61,7 @@ constexpr int NBR = 2048;                    // radix-select digit bins (11 bits
 constexpr int SUB_SHIFT = 34;                // level-2 bin = bits 45..34 inside a level-1 bin
 constexpr int SLOTS = 8;                     // candidates kept per level-2 bin
 constexpr int NB2 = 4096;                    // level-2 histogram: bits 47..36 inside a bin
-constexpr int CHUNK = 16384;                 // pixels per collect/apply task (< 65536)
+constexpr int CHUNK = 16384;                 // values per collect/apply task (< 65536)
 constexpr int RING = 16;                     // candidate buffers / level-2 histograms in flight
 constexpr int SEL_CAP = GR * GWP + BR * BWP;  // doubles of smem the select may use
 
@@ -315,6 +315,28 @@ __device__ void band_gray(const Params& p, Smem& s, int v, int x0, int y_first, 
 // computed at the clamped column), rows h*8 .. h*8+7, streaming the input rows top to bottom
 // so every output sums its taps in NI_Correlate's row-major order.  Rows outside the image
 // take the value of the clamped in-image row (mode="nearest" on the blurred image).
+// Blurred rows outside the image take the value of the clamped in-image row (mode="nearest"
+// on the blurred image): computed directly at the clamped row (band edges only).
+template <bool FAST, int CH>
+__device__ __noinline__ void blur_edge_rows(const Params& p, const double* gin, double* bout,
+                                            int y0, int nr) {
+  const int H = (int)p.H;
+  for (int o = 0; o < nr; ++o) {
+    const int y = y0 + o;
+    if (y >= 0 && y < H) continue;
+    const double* row = gin + (o + (clamp_i(y, 0, H - 1) - y)) * GWP;
+    double a = 0.0;
+    for (int di = 0; di < 5; ++di)
+      for (int dj = 0; dj < 5; ++dj) {
+        const int t25 = di * 5 + dj;
+        const double w = p.w25[t25];
+        if (FAST) a = (t25 == 0) ? row[di * GWP + dj] * w : a + row[di * GWP + dj] * w;
+        else if ((p.keep_mask >> t25) & 1u) a = a + row[di * GWP + dj] * w;
+      }
+    bout[o * BWP] = (CH == 3) ? (a > 1.0 ? 1.0 : a) : np_clip01_int(a);
+  }
+}
+
 template <bool FAST, int CH>
 __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_first, int cnt) {
   const int c = threadIdx.x & 127, h = threadIdx.x >> 7;
@@ -332,12 +354,14 @@ __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_
     double xv[5];
 #pragma unroll
     for (int dj = 0; dj < 5; ++dj) xv[dj] = gin[r * GWP + dj];
+    // innermost over the outputs: consecutive adds go to independent accumulators; each
+    // output still sums its taps in row-major (di, dj) order
 #pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      const int di = r - o;
-      if (di < 0 || di > 4) continue;
+    for (int dj = 0; dj < 5; ++dj) {
 #pragma unroll
-      for (int dj = 0; dj < 5; ++dj) {
+      for (int o = 0; o < 8; ++o) {
+        const int di = r - o;
+        if (di < 0 || di > 4) continue;
         const int t25 = di * 5 + dj;
         if (FAST) {
           const double prod = xv[dj] * wsym(di, dj);
@@ -359,25 +383,7 @@ __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_
     for (int o = 0; o < 8; ++o)
       if (o < nr) bout[o * BWP] = finish(acc[o]);
   }
-  if (y0 < 0 || y0 + nr > H) {  // rare: top / bottom rows of the image
-    for (int o = 0; o < nr; ++o) {
-      const int y = y0 + o;
-      if (y >= 0 && y < H) continue;
-      const double* row = gin + (o + (clamp_i(y, 0, H - 1) - y)) * GWP;
-      double a = 0.0;
-      for (int di = 0; di < 5; ++di)
-        for (int dj = 0; dj < 5; ++dj) {
-          const int t25 = di * 5 + dj;
-          if (FAST) {
-            const double prod = row[di * GWP + dj] * wsym(di, dj);
-            a = (t25 == 0) ? prod : a + prod;
-          } else if ((p.keep_mask >> t25) & 1u) {
-            a = a + row[di * GWP + dj] * p.w25[t25];
-          }
-        }
-      bout[o * BWP] = finish(a);
-    }
-  }
+  if (y0 < 0 || y0 + nr > H) blur_edge_rows<FAST, CH>(p, gin, bout, y0, nr);  // rare
 }
 
 __device__ __forceinline__ void sobel_at(const double* t, const double* m, const double* d,
@@ -446,12 +452,9 @@ __device__ void band_sobel(const Params& p, Smem& s, int x0, int y_first, int rq
       m[k] = d[k];
     }
   };
-  if (nr == 8 && y0 >= 0 && y0 + 8 <= H) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) row(j, false);
-  } else {
-    for (int j = 0; j < nr; ++j) row(j, true);
-  }
+  for (int j = 0; j < 8; ++j)
+    if (j < nr) row(j, true);
 }
 
 // Exact glibc hypot at magnitude cell (s.q row rq, column c) of image row y (0 outside).
@@ -634,7 +637,7 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
 }
 
 // ------------------------------------------------ histogram-only chunk (median-only mode)
-__device__ void run_hist_chunk(const Params& p, Smem& s, int v, int c) {
+__device__ __noinline__ void run_hist_chunk(const Params& p, Smem& s, int v, int c) {
   const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, p.npx);
   const double* src = (const double*)p.img + (long long)v * p.npx;
   for (long long i = lo + threadIdx.x; i < hi; i += NT) {
@@ -660,7 +663,7 @@ __device__ void flush_hist(const Params& p, Smem& s, int v) {
 // Locate the bin holding rank `rank` in a histogram of nb bins (nb % NT == 0, <= 16 * NT).
 // Every thread returns the same (bin, rank within bin) via smem.
 template <int NBINS>
-__device__ void locate(const unsigned* h, Smem& s, unsigned long long rank, int& bin,
+__device__ __noinline__ void locate(const unsigned* h, Smem& s, unsigned long long rank, int& bin,
                        unsigned long long& rin, bool global_mem) {
   constexpr int PER = NBINS / NT;
   unsigned loc[PER], sum = 0;
@@ -687,7 +690,7 @@ __device__ void locate(const unsigned* h, Smem& s, unsigned long long rank, int&
 }
 
 // Last E task of a view: locate the level-1 bins holding ranks k1 = (n-1)/2 and k2 = n/2.
-__device__ void find_median_bins(const Params& p, Smem& s, int v) {
+__device__ __noinline__ void find_median_bins(const Params& p, Smem& s, int v) {
   const unsigned* gh = p.hist + (long long)v * NB;
   constexpr int PER = NB / NT;
   unsigned local = 0;
@@ -806,7 +809,7 @@ __device__ __forceinline__ void stage(Smem& s, double x, int list, double* overf
   }
 }
 
-__device__ void run_collect(const Params& p, Smem& s, int v, int c) {
+__device__ __noinline__ void run_collect(const Params& p, Smem& s, int v, int c) {
   ViewCtl& ctl = p.ctl[v];
   if (threadIdx.x == 0) {  // claimed only once binfound (and the ring slot) is published
     s.ivals[0] = __ldcg(&ctl.npos) ? 1 : 0;
@@ -857,7 +860,7 @@ __device__ void run_collect(const Params& p, Smem& s, int v, int c) {
 
 // Block-wide radix select over n positive doubles (bit order == value order) stored at
 // src[dir * i] (global or shared).  Bits above `top` are already known to be equal.
-__device__ unsigned long long block_radix_select(Smem& s, const double* src, long long n, int dir,
+__device__ __noinline__ unsigned long long block_radix_select(Smem& s, const double* src, long long n, int dir,
                                                  unsigned long long rank, int top, bool global_mem) {
   unsigned long long prefix = 0, pmask = top >= 63 ? 0ull : (~0ull << (top + 1));
   unsigned* h = s.hist;  // reused; cleared on exit
@@ -906,7 +909,7 @@ struct Want {
   unsigned cnt;
 };
 
-__device__ void gather_subbins(Smem& s, const double* src, long long n, int dir, int sbA,
+__device__ __noinline__ void gather_subbins(Smem& s, const double* src, long long n, int dir, int sbA,
                                double* bufA, int sbB, double* bufB) {
   constexpr int U = 8;
   for (long long base = 0; base < n; base += NT * U) {
@@ -928,7 +931,7 @@ __device__ void gather_subbins(Smem& s, const double* src, long long n, int dir,
 
 // Rank selection for a short shared-memory list (n <= NT): element t's rank is the number of
 // smaller elements plus equal ones before it; the owner of rank `rank` publishes its bits.
-__device__ unsigned long long small_select(Smem& s, const double* buf, int n,
+__device__ __noinline__ unsigned long long small_select(Smem& s, const double* buf, int n,
                                            unsigned long long rank) {
   const int t = threadIdx.x;
   if (t < n) {
@@ -946,13 +949,13 @@ __device__ unsigned long long small_select(Smem& s, const double* buf, int n,
   return res;
 }
 
-__device__ unsigned long long select_staged(Smem& s, const double* buf, unsigned n,
+__device__ __noinline__ unsigned long long select_staged(Smem& s, const double* buf, unsigned n,
                                             unsigned long long rank) {
   if (n <= (unsigned)NT) return small_select(s, buf, (int)n, rank);
   return block_radix_select(s, buf, n, 1, rank, 35, false);
 }
 
-__device__ void plan(Smem& s, Want& w) {
+__device__ __noinline__ void plan(Smem& s, Want& w) {
   w.sb = -1;
   if (w.bin == 0 || w.bin == NB - 1) return;
   int sb;
@@ -966,7 +969,7 @@ __device__ void plan(Smem& s, Want& w) {
 // Order statistic of one Want: from the bucketed slots when the level-2 bin holds at most
 // SLOTS candidates (the common case: ~1 per bin), else by staging the level-2 bin from the
 // flat candidate list, else (clamped level-1 bin) by a full-width select over the list.
-__device__ double resolve(Smem& s, const Want& w, const double* slots) {
+__device__ __noinline__ double resolve(Smem& s, const Want& w, const double* slots) {
   if (w.sb < 0)
     return __longlong_as_double(block_radix_select(s, w.src, w.n, w.dir, w.rank, 63, true));
   double* buf = s.g;
@@ -987,7 +990,7 @@ __device__ double resolve(Smem& s, const Want& w, const double* slots) {
   return __longlong_as_double(select_staged(s, buf, w.cnt, w.r2));
 }
 
-__device__ void run_select(const Params& p, Smem& s, int v) {
+__device__ __noinline__ void run_select(const Params& p, Smem& s, int v) {
   ViewCtl& ctl = p.ctl[v];
   const int slot = v % RING;
   const double* cand = cand_lists(p, v);
@@ -1034,7 +1037,7 @@ __device__ __forceinline__ double normalise(double x, double denom, double rd, b
   return np_min1(q);
 }
 
-__device__ void run_apply(const Params& p, Smem& s, int v, int c, unsigned long long pol_out) {
+__device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, unsigned long long pol_out) {
   ViewCtl& ctl = p.ctl[v];  // claimed only once select_done is published
   const double denom = __ldcg(&ctl.denom);
   const double rd = __drcp_rn(denom);
@@ -1188,7 +1191,7 @@ __device__ void claim_next(const Params& p, Smem& s, unsigned long long pol_in) 
 }
 
 template <bool FAST, int CH, bool F64>
-__global__ void __launch_bounds__(NT, 3) edge_persistent_kernel(Params p) {
+__global__ void __launch_bounds__(NT, 3) edge_persistent_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   for (int i = threadIdx.x; i < NB / 2; i += NT) s.hist[i] = 0;

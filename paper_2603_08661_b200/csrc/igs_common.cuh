@@ -106,7 +106,21 @@ __device__ __forceinline__ double hypot_kernel(double ax, double ay) {
   return h - (t1 + t2) / (h + h);
 }
 
+static __device__ __noinline__ double hypot_glibc_slow(double x, double y);
+
+// glibc hypot: the common range inline, the scaled / non-finite / trivial cases out of line.
 __device__ __forceinline__ double hypot_glibc(double x, double y) {
+  double ax = fabs(x), ay = fabs(y);
+  if (ax < ay) {
+    double t = ax;
+    ax = ay;
+    ay = t;
+  }
+  if (ay >= 0x1p-459 && ax <= 0x1p+511 && ay > ax * 0x1p-54) return hypot_kernel(ax, ay);
+  return hypot_glibc_slow(x, y);
+}
+
+static __device__ __noinline__ double hypot_glibc_slow(double x, double y) {
   double ax = fabs(x), ay = fabs(y);
   if (!isfinite(ax) || !isfinite(ay)) {
     if (isinf(ax) || isinf(ay)) return __longlong_as_double(0x7ff0000000000000LL);
@@ -130,60 +144,6 @@ __device__ __forceinline__ double hypot_glibc(double x, double y) {
   return hypot_kernel(ax, ay);
 }
 
-// Reciprocal to ~full double precision (NOT correctly rounded): MUFU seed + two Newton steps.
-__device__ __forceinline__ double rcp_nr(double d) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  return fma(r, e, r);
-}
-
-// hypot_kernel with the correction quotient (t1+t2)/(2h) from rcp_nr instead of an IEEE
-// division.  The correction is below one ulp of h, so a relative error of ~2^-52 in it can
-// change fl(h - q) only when h - q lies within ~2^-51 ulp(h) of a rounding boundary.  The
-// sqrt and t1, t2 keep glibc's exact operation order.
-__device__ __forceinline__ double hypot_kernel_fast(double ax, double ay) {
-  double h = sqrt(ax * ax + ay * ay);
-  double t1, t2;
-  if (h <= ay + ay) {
-    double d = h - ay;
-    t1 = ((d + d) - ax) * ax;
-    double two_diff = (ax - ay) + (ax - ay);
-    t2 = (d - two_diff) * d;
-  } else {
-    double d = h - ax;
-    t1 = (d + d) * (ax - (ay + ay));
-    t2 = ((4.0 * d) - ay) * ay + d * d;
-  }
-  return h - (t1 + t2) * rcp_nr(h + h);
-}
-
-__device__ __forceinline__ double hypot_glibc_fast(double x, double y) {
-  double ax = fabs(x), ay = fabs(y);
-  if (ax < ay) {
-    double t = ax;
-    ax = ay;
-    ay = t;
-  }
-  // common case first: 2^-459 <= ay, ax <= 2^511 and ay > ax * 2^-54
-  if (ay >= 0x1p-459 && ax <= 0x1p+511 && ay > ax * 0x1p-54) return hypot_kernel_fast(ax, ay);
-  return hypot_glibc(x, y);
-}
-
-// Same for |x|, |y| <= 2^511 (Sobel of an RGB-derived gray in [0, 1]: |g| <= 4).
-__device__ __forceinline__ double hypot_glibc_fast_bounded(double x, double y) {
-  double ax = fabs(x), ay = fabs(y);
-  if (ax < ay) {
-    double t = ax;
-    ax = ay;
-    ay = t;
-  }
-  if (ay >= 0x1p-459 && ay > ax * 0x1p-54) return hypot_kernel_fast(ax, ay);
-  return hypot_glibc(x, y);
-}
-
 // np.clip(x, 0, 1) on the bit pattern (integer pipe): NaN kept, x <= 0 (incl. -0) -> +0.
 __device__ __forceinline__ double np_clip01_int(double x) {
   long long b = __double_as_longlong(x);
@@ -202,7 +162,7 @@ __device__ __forceinline__ double div_by(double x, double d, double rd) {
 // NMS direction bin of the gradient (gx, gy) -- identical to
 // np_orientation_bin(np_mod(atan2(gy, gx), pi)) except within ~1e-12 rad of a
 // bin boundary, where it falls back to evaluating that expression.
-__device__ __forceinline__ int gradient_bin(double gx, double gy) {
+static __device__ __noinline__ int gradient_bin(double gx, double gy) {
   double ax = fabs(gx), ay = fabs(gy);
   if (ay == 0.0) return 0;         // theta in {0, pi, -pi} -> folded to 0 -> bin 0
   if (ax == 0.0 && isfinite(ay)) return 2;  // theta = +-pi/2 -> pi/2 -> bin 2
@@ -217,23 +177,6 @@ __device__ __forceinline__ int gradient_bin(double gx, double gy) {
   if (d0 < 0.0) return 0;
   if (d2 < 0.0) return 2;
   return ((gx > 0.0) == (gy > 0.0)) ? 1 : 3;
-}
-
-// gradient_bin with the common case first: no zero tests (an axis-aligned gradient is decided
-// by the same margin test), the quadrant from the sign bits.  Exactly zero, near-boundary and
-// non-finite gradients take gradient_bin.
-__device__ __forceinline__ int gradient_bin_fast(double gx, double gy) {
-  const double kTan = 0.41421356237309503;  // tan(pi/8)
-  const double ax = fabs(gx), ay = fabs(gy);
-  const double d0 = fma(-kTan, ax, ay);
-  const double d2 = fma(-kTan, ay, ax);
-  const double tol = 1e-12 * (ax + ay);
-  if (fabs(d0) > tol && fabs(d2) > tol) {
-    if (d0 < 0.0) return 0;
-    if (d2 < 0.0) return 2;
-    return ((__double2hiint(gx) ^ __double2hiint(gy)) >= 0) ? 1 : 3;
-  }
-  return gradient_bin(gx, gy);
 }
 
 // ---- block helpers ----------------------------------------------------------
