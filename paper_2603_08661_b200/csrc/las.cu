@@ -112,6 +112,31 @@ __global__ void __launch_bounds__(1024) las_scan_kernel(const unsigned* tile_cnt
   if (threadIdx.x == 0) summary[0] = carry;
 }
 
+// Clone the SH rows (Q4 float4 each) of a tile's compacted parents src_idx[0..n) to the
+// consecutive appended rows slot0 ..: 16-byte streaming loads, U in flight per thread.
+template <int Q4>
+__device__ __forceinline__ void clone_rows(float* sh, const long long* src_idx, unsigned n,
+                                           unsigned long long slot0) {
+  constexpr int U = 4;
+  const float4* src = reinterpret_cast<const float4*>(sh);
+  float4* dstp = reinterpret_cast<float4*>(sh);
+  const unsigned total = n * Q4;
+  for (unsigned e0 = threadIdx.x; e0 < total; e0 += U * NT) {
+    float4 v[U];
+    unsigned k[U], qq[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned e = e0 + u * NT;
+      k[u] = e / Q4;
+      qq[u] = e - k[u] * Q4;
+      if (e < total) v[u] = ld_stream_f4(src + src_idx[k[u]] * Q4 + qq[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * NT < total) __stcs(dstp + (long long)(slot0 + k[u]) * Q4 + qq[u], v[u]);
+  }
+}
+
 struct Consts {
   float alpha, log_alpha, log_gamma, beta;
 };
@@ -223,7 +248,11 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
   // SH clone of the tile's parents into consecutive appended rows.
   const unsigned n = s_total;
   if (n == 0 || sh_floats == 0) return;
-  if ((sh_floats & 3) == 0) {
+  if (sh_floats == 48) {  // SH degree 3: 12 float4 per row, four loads in flight per thread
+    clone_rows<12>(sh, src_idx, n, slot0);
+  } else if (sh_floats == 12) {  // SH degree 1
+    clone_rows<3>(sh, src_idx, n, slot0);
+  } else if ((sh_floats & 3) == 0) {
     const long long q4 = sh_floats >> 2;
     const float4* src = reinterpret_cast<const float4*>(sh);
     float4* dstp = reinterpret_cast<float4*>(sh);

@@ -154,13 +154,15 @@ __global__ void __launch_bounds__(NT) hist_kernel(const unsigned long long* __re
   smem_hist_flush(h, hist);
 }
 
-// One block: digit of rank st->rank in the merged histogram of `round`.
+// One block: digit of rank st->rank in the merged histogram of `round`.  Warp w owns the
+// contiguous bins [w * 2048, (w + 1) * 2048): coalesced loads, warp sums, a scan of the 32
+// warp totals, then the owning warp resolves the bin with ballots (no per-thread arrays).
 __global__ void __launch_bounds__(NT) resolve_kernel(const int* __restrict__ hist, int round,
                                                      long long take_cap, State* st,
                                                      long long* counts) {
-  __shared__ unsigned warp_sums[32];
-  __shared__ int s_digit;
+  __shared__ unsigned warp_tot[32];
   __shared__ unsigned long long s_rank;
+  __shared__ int s_warp;
   if (round == 0) {
     if (threadIdx.x == 0) {
       const unsigned long long ne = (unsigned long long)(unsigned)hist[NBINS];
@@ -182,35 +184,65 @@ __global__ void __launch_bounds__(NT) resolve_kernel(const int* __restrict__ his
     __syncthreads();
   }
   if (st->status) return;
-  constexpr int PER = NBINS / NT;
-  unsigned loc[PER], sum = 0;
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    loc[k] = (unsigned)hist[threadIdx.x * PER + k];
-    sum += loc[k];
-  }
-  unsigned total;
-  const unsigned before = block_exclusive_scan(sum, warp_sums, &total);
+  constexpr int PERW = NBINS / (NT / 32);  // 2048 bins per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int* h = hist + warp * PERW;
+  unsigned sum = 0;
+#pragma unroll 8
+  for (int i = lane; i < PERW; i += 32) sum += (unsigned)h[i];
+  sum = __reduce_add_sync(0xffffffffu, sum);
+  if (lane == 0) warp_tot[warp] = sum;
+  __syncthreads();
   const unsigned long long rank = st->rank;
-  unsigned long long cum = before;
+  if (warp == 0) {
+    unsigned x = warp_tot[lane], inc = x;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    if (loc[k] && rank >= cum && rank < cum + loc[k]) {
-      s_digit = threadIdx.x * PER + k;
-      s_rank = rank - cum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
     }
-    cum += loc[k];
+    const unsigned long long ex = inc - x;
+    const bool mine = x && rank >= ex && rank < ex + x;
+    const unsigned b = __ballot_sync(0xffffffffu, mine);
+    const int w = __ffs(b) - 1;
+    if (lane == w) {
+      s_warp = w;
+      s_rank = rank - ex;
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const int sh = round_shift(round);
-    st->prefix |= (unsigned long long)s_digit << sh;
-    st->pmask |= 0xffffull << sh;
-    st->rank = s_rank;
-    if (round == ROUNDS - 1) {
-      st->T = st->prefix;
-      st->need_ties = s_rank + 1;
+  if (warp != s_warp) return;
+  // the owning warp walks its 2048 bins 32 at a time
+  unsigned long long r = s_rank;
+  const int* hw = hist + warp * PERW;
+  for (int base = 0; base < PERW; base += 32) {
+    const unsigned c = (unsigned)hw[base + lane];
+    unsigned inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
     }
+    const unsigned tot = __shfl_sync(0xffffffffu, inc, 31);
+    if (r < tot) {
+      const unsigned long long ex = inc - c;
+      const bool mine = c && r >= ex && r < ex + c;
+      const unsigned b = __ballot_sync(0xffffffffu, mine);
+      const int l = __ffs(b) - 1;
+      if (lane == l) {
+        const int digit = warp * PERW + base + l;
+        const int sh = round_shift(round);
+        st->prefix |= (unsigned long long)digit << sh;
+        st->pmask |= 0xffffull << sh;
+        st->rank = r - ex;
+        if (round == ROUNDS - 1) {
+          st->T = st->prefix;
+          st->need_ties = r - ex + 1;
+        }
+      }
+      return;
+    }
+    r -= tot;
   }
 }
 
