@@ -90,6 +90,15 @@ int igs_median_normalize(const double* in, int64_t batch, int64_t n, double* out
                          double* medians, void* workspace, size_t workspace_bytes,
                          void* stream);
 
+/* sample_scores (edge_pipeline.py:138-164): bilinear samples of importance maps at
+ * positions (n, 2) float64 (x, y) -- 16-byte aligned -- of map view[i] (view nullable: map 0)
+ * of maps (batch, height, width) float64; outside [0, W-1] x [0, H-1] -> 0.  flags (device
+ * int32) receives bit 1 for a NaN position (the reference raises IndexError), bit 2 for a
+ * view index outside [0, batch). */
+int igs_sample_scores(const double* maps, int64_t batch, int64_t height, int64_t width,
+                      const double* positions, const int32_t* view, int64_t n, double* scores,
+                      int32_t* flags, void* stream);
+
 /* Debug: record {start_ns, end_ns, kind, view, index, smid} (32 bytes) per task of later
  * igs_edge_importance launches into the device buffer buf (NULL disables); *written (nullable)
  * receives the number of records the previous launches produced. */

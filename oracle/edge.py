@@ -194,3 +194,31 @@ def importance_batch(images, sigma=1.0):
     """Per-view pipeline over a (B, H, W, 3) or (B, H, W) stack (per-image medians)."""
     images = np.asarray(images)
     return np.stack([importance_pipeline(im, sigma) for im in images])
+
+
+def sample_scores(importance, positions):
+    """edge_pipeline.py:138-164: bilinear sample at (x, y); outside [0, W-1] x [0, H-1] -> 0.
+
+    value = ((1 - fy) * ((1 - fx) v00 + fx v01)) + (fy * ((1 - fx) v10 + fx v11)), each
+    product and sum rounded separately (numpy evaluates the expression left to right).
+    NaN positions make numpy index with INT64_MIN: the reference raises IndexError.
+    """
+    importance = np.asarray(importance, dtype=np.float64)
+    positions = np.asarray(positions, dtype=np.float64).reshape(-1, 2)
+    h, w = importance.shape
+    x, y = positions[:, 0], positions[:, 1]
+    if np.isnan(positions).any():
+        raise IndexError("NaN sample position")
+    inside = (x >= 0.0) & (x <= w - 1.0) & (y >= 0.0) & (y <= h - 1.0)
+    xc = np.minimum(np.maximum(x, 0.0), w - 1.0)
+    yc = np.minimum(np.maximum(y, 0.0), h - 1.0)
+    x0 = np.floor(xc).astype(np.int64)
+    y0 = np.floor(yc).astype(np.int64)
+    x1 = np.minimum(x0 + 1, w - 1)
+    y1 = np.minimum(y0 + 1, h - 1)
+    fx = xc - x0
+    fy = yc - y0
+    top = (1 - fx) * importance[y0, x0] + fx * importance[y0, x1]
+    bot = (1 - fx) * importance[y1, x0] + fx * importance[y1, x1]
+    value = (1 - fy) * top + fy * bot
+    return np.where(inside, value, 0.0)

@@ -13,7 +13,7 @@ from .densify_controller import (EVENT_CSV_HEADER, DensifyEvent, DensifyStats,
                                  accumulate_grads, densify_step, select_candidates)
 from .edge_pipeline import (GradientField, blur_kernel_5x5, gaussian_blur_5x5,
                             importance_batch, importance_pipeline, median_normalize,
-                            nms_thin, sobel_gradients, to_grayscale)
+                            nms_thin, sample_scores, sobel_gradients, to_grayscale)
 from .las_split import BudgetError, SplitConstants, las_split_batch, principal_axis
 from .schedule import DensifyConfig, is_densify_step, is_warmup_step
 

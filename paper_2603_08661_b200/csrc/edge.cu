@@ -43,7 +43,14 @@ namespace edge {
 
 constexpr int NT = 256;                      // threads per block
 constexpr int NWARP = NT / 32;
-constexpr int SR = 16;                       // output rows per band sub-step
+#ifndef IGS_SR
+#define IGS_SR 16
+#endif
+constexpr int SR = IGS_SR;                   // output rows per band sub-step
+constexpr int SH = SR / 2;                   // rows per blur / Sobel strip (two strips)
+#ifndef IGS_MINB
+#define IGS_MINB 3
+#endif
 constexpr int TWM = 124;                     // max output columns per band
 constexpr int BAND_H = 128;                  // max rows per band (tuning override)
 constexpr int BAND_H_DEFAULT = 64;           // rows per band
@@ -51,7 +58,7 @@ constexpr int GWP = TWM + 8, BWP = 128, MWP = 128;  // row pitches (cells); the 
                                                     // Sobel lanes cover 128 columns
 constexpr int GR = SR + 8, BR = SR + 4, QR = SR + 2;        // rows per sub-step + context
 static_assert(TWM * BAND_H < 65536, "16-bit shared histogram counters per band");
-static_assert(TWM + 4 <= 128 && 2 * 8 == SR, "blur / Sobel: 128 columns x 2 strips of 8 rows");
+static_assert(TWM + 4 <= 128 && 2 * SH == SR && SR <= 16, "blur / Sobel: 128 columns x 2 strips");
 static_assert(TWM + 8 <= 132, "gray: 4 x 32 lanes + 4 columns");
 
 constexpr int NB = 4096;                     // level-1 median histogram: 64 bins per octave
@@ -130,7 +137,7 @@ struct __align__(16) Smem {
   double g[GR * GWP];       // gray rows of a band sub-step; C/A stream buffers, select scratch
   double b[BR * BWP];       // blurred rows (contiguous with g)
   unsigned q[QR * MWP];     // Sobel cells: (|grad|^2 key << 2) | direction bin
-  unsigned list[SR * TWM];  // compacted NMS survivors / undecided pixels of a sub-step
+  unsigned short list[SR * TWM];  // compacted NMS survivors / undecided pixels of a sub-step
   unsigned list_n[2];       // list lengths (double-buffered by sub-step parity)
   unsigned hist[NB / 2];    // level-1 counts packed two 16-bit bins per word; radix scratch
   unsigned warp_sums[32];
@@ -341,16 +348,16 @@ template <bool FAST, int CH>
 __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_first, int cnt) {
   const int c = threadIdx.x & 127, h = threadIdx.x >> 7;
   const int H = (int)p.H, W = (int)p.W;
-  const int r0 = h * 8;
+  const int r0 = h * SH;
   if (r0 >= cnt) return;
-  const int nr = min(8, cnt - r0);
+  const int nr = min(SH, cnt - r0);
   const int gc = clamp_i(x0 - 2 + c, 0, W - 1) - x0 + 2;  // s.g column of the leftmost tap
   const double* gin = s.g + (rb_first + r0) * GWP + gc;
   auto wsym = [&](int di, int dj) { return p.w6[di < 2 ? 2 - di : di - 2][dj < 2 ? 2 - dj : dj - 2]; };
   auto finish = [&](double x) { return (CH == 3) ? (x > 1.0 ? 1.0 : x) : np_clip01_int(x); };
-  double acc[8];
+  double acc[SH];
 #pragma unroll
-  for (int r = 0; r < 12; ++r) {
+  for (int r = 0; r < SH + 4; ++r) {
     double xv[5];
 #pragma unroll
     for (int dj = 0; dj < 5; ++dj) xv[dj] = gin[r * GWP + dj];
@@ -359,7 +366,7 @@ __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_
 #pragma unroll
     for (int dj = 0; dj < 5; ++dj) {
 #pragma unroll
-      for (int o = 0; o < 8; ++o) {
+      for (int o = 0; o < SH; ++o) {
         const int di = r - o;
         if (di < 0 || di > 4) continue;
         const int t25 = di * 5 + dj;
@@ -375,12 +382,12 @@ __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_
   }
   double* bout = s.b + (rb_first + r0) * BWP + c;
   const int y0 = y_first + r0;
-  if (nr == 8) {
+  if (nr == SH) {
 #pragma unroll
-    for (int o = 0; o < 8; ++o) bout[o * BWP] = finish(acc[o]);
+    for (int o = 0; o < SH; ++o) bout[o * BWP] = finish(acc[o]);
   } else {
 #pragma unroll
-    for (int o = 0; o < 8; ++o)
+    for (int o = 0; o < SH; ++o)
       if (o < nr) bout[o * BWP] = finish(acc[o]);
   }
   if (y0 < 0 || y0 + nr > H) blur_edge_rows<FAST, CH>(p, gin, bout, y0, nr);  // rare
@@ -422,9 +429,9 @@ template <bool NMS>
 __device__ void band_sobel(const Params& p, Smem& s, int x0, int y_first, int rq_first, int cnt) {
   const int c = threadIdx.x & 127, h = threadIdx.x >> 7;
   const int H = (int)p.H, W = (int)p.W;
-  const int r0 = h * 8;
+  const int r0 = h * SH;
   if (r0 >= cnt) return;
-  const int nr = min(8, cnt - r0);
+  const int nr = min(SH, cnt - r0);
   const int x = x0 - 1 + c;
   const bool xin = x >= 0 && x < W;
   const int y0 = y_first + r0;
@@ -453,7 +460,7 @@ __device__ void band_sobel(const Params& p, Smem& s, int x0, int y_first, int rq
     }
   };
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < SH; ++j)
     if (j < nr) row(j, true);
 }
 
@@ -470,7 +477,7 @@ __device__ __forceinline__ double mag_exact(const Params& p, const Smem& s, int 
 
 // NMS decisions of output rows [y_first, y_first + cnt) (s.q row r + 1): warp w rows w and
 // w + NWARP, lane l columns l + 32 k.  Suppressed pixels store 0 here; survivors and
-// undecided pixels are appended to s.list as (r << 16) | (c << 4) | (undecided prev << 1) |
+// undecided pixels are appended to s.list as (r << 12) | (c << 2) | (undecided prev << 1) |
 // undecided next (warp-aggregated).
 __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw, int y_first,
                                 int cnt, int parity) {
@@ -500,10 +507,10 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
         // suppressed for sure: prev decided >= self, or next decided > self
         const bool rej = (!u1 && d1 <= 0) || (!u2 && d2 < 0);
         need = !rej;
-        entry = ((unsigned)r << 16) | ((unsigned)c << 4) | (u1 ? 2u : 0u) | (u2 ? 1u : 0u);
+        entry = ((unsigned)r << 12) | ((unsigned)c << 2) | (u1 ? 2u : 0u) | (u2 ? 1u : 0u);
       } else {
         need = (qc >> 2) != 0;
-        entry = ((unsigned)r << 16) | ((unsigned)c << 4);
+        entry = ((unsigned)r << 12) | ((unsigned)c << 2);
       }
       need = need && c < xw;
       if (!need && c < xw) orow[c] = 0.0;
@@ -512,7 +519,7 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(&s.list_n[parity], (unsigned)__popc(bal));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (need) s.list[base + __popc(bal & lanemask_lt())] = entry;
+        if (need) s.list[base + __popc(bal & lanemask_lt())] = (unsigned short)entry;
       }
     }
   }
@@ -533,7 +540,7 @@ __device__ void band_nms_finish(const Params& p, Smem& s, int v, int x0, int y_f
     unsigned pix = 0;
     if (i < n) {
       const unsigned e = s.list[i];
-      const int r = (int)(e >> 16), c = (int)((e >> 4) & 0xfffu);
+      const int r = (int)(e >> 12), c = (int)((e >> 2) & 0x3ffu);
       const int y = y_first + r;
       const double m = mag_exact(p, s, x0, y, r + 1, c + 1);
       bool keep = true;
@@ -1191,7 +1198,7 @@ __device__ void claim_next(const Params& p, Smem& s, unsigned long long pol_in) 
 }
 
 template <bool FAST, int CH, bool F64>
-__global__ void __launch_bounds__(NT, 3) edge_persistent_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(NT, IGS_MINB) edge_persistent_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   for (int i = threadIdx.x; i < NB / 2; i += NT) s.hist[i] = 0;

@@ -228,6 +228,42 @@ def importance_batch(images, sigma: float = 1.0, *, out=None, nms: bool = True,
     return _ret(out, np_out)
 
 
+def sample_scores(importance, positions, view=None):
+    """Bilinearly sample an importance map at (x, y) pixel positions (edge_pipeline.py:138-164);
+    positions outside [0, W-1] x [0, H-1] score 0.  Batched form: ``importance`` (B, H, W) and
+    ``view`` (N,) int map indices.  numpy in -> numpy out; CUDA tensors -> CUDA tensor."""
+    imp, np_out = _as_cuda(importance)
+    pos, _ = _as_cuda(positions)
+    if imp.ndim == 2:
+        imp = imp.unsqueeze(0)
+    if imp.ndim != 3:
+        raise ValueError("importance must be (H, W) or (B, H, W)")
+    pos = pos.reshape(-1, 2).contiguous()
+    if pos.data_ptr() % 16:
+        pos = pos.clone()
+    n = pos.shape[0]
+    vw = None
+    if view is not None:
+        vw = torch.as_tensor(np.asarray(view) if not isinstance(view, torch.Tensor) else view)
+        vw = vw.to(imp.device, torch.int32).reshape(-1).contiguous()
+        if vw.shape[0] != n:
+            raise ValueError("view must have one entry per position")
+    elif imp.shape[0] != 1:
+        raise ValueError("batched importance maps need a view index per position")
+    out = torch.empty(n, dtype=torch.float64, device=imp.device)
+    flags = torch.zeros(1, dtype=torch.int32, device=imp.device)
+    L = _lib.lib()
+    _lib.check(L.igs_sample_scores(imp.data_ptr(), imp.shape[0], imp.shape[1], imp.shape[2],
+                                   pos.data_ptr(), _lib.ptr(vw), n, out.data_ptr(),
+                                   flags.data_ptr(), _lib.stream_handle()), "sample_scores")
+    f = int(flags.item()) if n else 0
+    if f & 1:
+        raise IndexError("NaN sample position (the reference indexes with INT64_MIN)")
+    if f & 2:
+        raise IndexError("view index out of range")
+    return _ret(out, np_out)
+
+
 def _batch_geometry(img):
     if img.ndim == 4:
         if img.shape[3] != 3:

@@ -24,7 +24,8 @@ from splitkit.densify_controller import (DensifyStats, accumulate_grads,  # noqa
                                          densify_step, select_candidates)
 from splitkit.edge_pipeline import (GradientField, gaussian_blur_5x5,  # noqa: E402
                                     importance_pipeline, median_normalize,
-                                    nms_thin, sobel_gradients, to_grayscale)
+                                    nms_thin, sample_scores, sobel_gradients,
+                                    to_grayscale)
 from splitkit.las_split import BudgetError, SplitConstants, las_split_batch  # noqa: E402
 from splitkit.schedule import DensifyConfig  # noqa: E402
 
@@ -250,9 +251,35 @@ def select_cases():
     return out
 
 
+def sample_cases():
+    """sample_scores (edge_pipeline.py:138-164): bilinear sampling, outside -> 0."""
+    out = {}
+    rng = np.random.default_rng(505)
+    maps = {
+        "rand10x12": rng.random((10, 12)),
+        "importance": importance_pipeline(synth_view(41, 57, 1003)),
+        "ramp": np.arange(12.0).reshape(3, 4),
+        "one_row": rng.random((1, 9)),
+        "one_col": rng.random((7, 1)),
+        "single": np.array([[0.75]]),
+    }
+    for name, imp in maps.items():
+        h, w = imp.shape
+        pos = np.column_stack([rng.uniform(-2, w + 1, 300), rng.uniform(-2, h + 1, 300)])
+        edge = np.array([[0.0, 0.0], [w - 1.0, h - 1.0], [w - 1.0, 0.0], [0.0, h - 1.0],
+                         [w - 1.0 + 1e-12, 0.0], [-1e-300, 0.0], [-0.0, -0.0],
+                         [(w - 1) / 2.0, (h - 1) / 2.0], [np.inf, 0.0], [0.0, -np.inf],
+                         [0.5, 0.25]])
+        pos = np.vstack([pos, edge, np.round(pos[:50] * 4) / 4])
+        out[f"{name}/map"] = imp
+        out[f"{name}/positions"] = pos
+        out[f"{name}/scores"] = sample_scores(imp, pos)
+    return out
+
+
 def main():
     for name, fn in (("edge", edge_cases), ("nms", nms_cases), ("median", median_cases),
-                     ("las", las_cases), ("select", select_cases)):
+                     ("las", las_cases), ("select", select_cases), ("sample", sample_cases)):
         data = fn()
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **data)
         print(name, len(data), "arrays")

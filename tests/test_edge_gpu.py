@@ -209,3 +209,32 @@ def test_crowded_median_bins():
     got = b.importance_batch(torch.from_numpy(views).cuda()).cpu().numpy()
     for v in range(views.shape[0]):
         assert_array_equal(got[v], OE.importance_pipeline(views[v]), err_msg=f"view {v}")
+
+
+def test_sample_scores_golden_bit_exact():
+    b = B()
+    for name, c in load_golden("sample").items():
+        assert_array_equal(b.sample_scores(c["map"], c["positions"]), c["scores"], err_msg=name)
+
+
+def test_sample_scores_large_batched_and_errors():
+    b = B()
+    from paper_2603_08661_b200.synth import synth_view
+    maps = np.stack([OE.importance_pipeline(synth_view(120, 170, 3000 + k)) for k in range(3)])
+    rng = np.random.default_rng(21)
+    n = 300_001
+    pos = np.column_stack([rng.uniform(-3, 172, n), rng.uniform(-3, 122, n)])
+    pos[::7] = np.round(pos[::7])           # integer (corner / edge) positions
+    view = rng.integers(0, 3, n)
+    got = b.sample_scores(torch.from_numpy(maps).cuda(), torch.from_numpy(pos).cuda(),
+                          view=view).cpu().numpy()
+    want = np.empty(n)
+    for k in range(3):
+        sel = view == k
+        want[sel] = OE.sample_scores(maps[k], pos[sel])
+    assert_array_equal(got, want)
+    with pytest.raises(IndexError):
+        b.sample_scores(maps[0], [[np.nan, 2.0]])
+    with pytest.raises(IndexError):
+        b.sample_scores(maps, pos[:4], view=[0, 1, 2, 3])
+    assert b.sample_scores(maps[0], np.zeros((0, 2))).shape == (0,)

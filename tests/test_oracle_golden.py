@@ -149,3 +149,21 @@ def test_select_known_answers():
     order_probe = np.array([0.5, np.nan, -0.0, 0.0, 0.5, np.inf, 0.25])
     m, _ = OS.select_candidates(np.ones(7), order_probe, True, "product", 0.0, 1.0, 3)
     assert_array_equal(np.flatnonzero(m), [0, 4, 5])
+
+
+def test_sample_scores_vectors():
+    for name, c in load_golden("sample").items():
+        assert_array_equal(OE.sample_scores(c["map"], c["positions"]), c["scores"], err_msg=name)
+
+
+def test_sample_scores_known_answers():
+    # pkg/tests/test_edge_pipeline.py:305-336
+    imp = np.zeros((4, 4))
+    imp[1, 1], imp[1, 2] = 0.2, 0.6
+    assert_allclose(OE.sample_scores(imp, [[1.5, 1.0]]), [0.4], rtol=1e-12)
+    assert_array_equal(OE.sample_scores(np.ones((8, 8)), [[-5.0, -5.0], [6.5, 3.0], [7.5, 3.0],
+                                                          [3.0, 8.0]]), [0.0, 1.0, 0.0, 0.0])
+    assert_array_equal(OE.sample_scores(np.arange(12.0).reshape(3, 4), [[0.0, 0.0], [3.0, 2.0]]),
+                       [0.0, 11.0])
+    with pytest.raises(IndexError):
+        OE.sample_scores(imp, [[np.nan, 1.0]])
