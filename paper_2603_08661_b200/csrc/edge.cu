@@ -144,7 +144,7 @@ struct __align__(16) Smem {
   int task_kind, task_view, task_idx, flag;
   int ivals[4];
   int scratch[4];
-  unsigned long long mbar[2];  // bulk-copy barriers of the C / A streams
+  unsigned long long mbar[4];  // bulk-copy barriers of the C / A streams (NBUF)
   unsigned long long u64[2];
 };
 
@@ -749,18 +749,18 @@ __device__ __forceinline__ int sub_bin(unsigned long long bits) {
 // A C/A task streams its chunk of the thinned map through shared memory in PIECE-sized
 // pieces with TMA bulk copies (two buffers in flight, mbarrier completion), so the task is
 // not limited by register-held loads.  Unaligned views fall back to plain loads.
-constexpr int PIECE = 2048;                     // doubles per piece (16 KB)
+constexpr int PIECE = 1536;                     // doubles per piece (12 KB)
+constexpr int NBUF = 4;                         // pieces in flight
 constexpr int STAGE = 256;                      // staged candidates per list in a C task
-static_assert(2 * PIECE + 2 * STAGE <= GR * GWP + BR * BWP, "stream buffers fit in g + b");
+static_assert(NBUF * PIECE + 2 * STAGE <= GR * GWP + BR * BWP + QR * MWP / 2,
+              "stream buffers fit in g + b + q");
 
-// g and b are contiguous doubles at the start of Smem: one arena for C/A/select scratch.
+// g, b and q are contiguous at the start of Smem: one arena for C/A/select scratch.
 __device__ __forceinline__ double* arena(Smem& s) { return reinterpret_cast<double*>(&s); }
 
 template <typename Visit>
 __device__ void stream_chunk(Smem& s, const double* src, long long lo, long long hi,
                              Visit visit) {
-  double* buf0 = arena(s);
-  double* buf1 = arena(s) + PIECE;
   const long long n = hi - lo;
   const bool aligned = ((((uintptr_t)(src + lo)) & 15) == 0);
   if (!aligned) {
@@ -769,31 +769,29 @@ __device__ void stream_chunk(Smem& s, const double* src, long long lo, long long
   }
   const long long nfull = n & ~1ll;  // bulk part: a multiple of 16 bytes
   const int npieces = (int)((nfull + PIECE - 1) / PIECE);
+  auto issue = [&](int k) {
+    const long long off = (long long)k * PIECE;
+    const unsigned len = (unsigned)min((long long)PIECE, nfull - off);
+    bulk_load(arena(s) + (k % NBUF) * PIECE, src + lo + off, len * 8u, &s.mbar[k % NBUF]);
+  };
   __syncthreads();
   if (threadIdx.x == 0) {
-    mbar_init(&s.mbar[0]);
-    mbar_init(&s.mbar[1]);
+    for (int k = 0; k < NBUF; ++k) mbar_init(&s.mbar[k]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
-    for (int k = 0; k < 2 && k < npieces; ++k) {
-      const long long off = (long long)k * PIECE;
-      const unsigned len = (unsigned)min((long long)PIECE, nfull - off);
-      bulk_load(k ? buf1 : buf0, src + lo + off, len * 8u, &s.mbar[k]);
-    }
+    for (int k = 0; k < NBUF && k < npieces; ++k) issue(k);
   }
   __syncthreads();
   for (int k = 0; k < npieces; ++k) {
-    double* buf = (k & 1) ? buf1 : buf0;
-    mbar_wait(&s.mbar[k & 1], (unsigned)((k >> 1) & 1));
+    const double* buf = arena(s) + (k % NBUF) * PIECE;
+    mbar_wait(&s.mbar[k % NBUF], (unsigned)((k / NBUF) & 1));
     const long long off = (long long)k * PIECE;
     const int len = (int)min((long long)PIECE, nfull - off);
     for (int i = threadIdx.x; i < len; i += NT) visit(lo + off + i, buf[i]);
     __syncthreads();
-    if (threadIdx.x == 0 && k + 2 < npieces) {
+    if (threadIdx.x == 0 && k + NBUF < npieces) {
       fence_proxy_async();
-      const long long o2 = (long long)(k + 2) * PIECE;
-      const unsigned l2 = (unsigned)min((long long)PIECE, nfull - o2);
-      bulk_load(buf, src + lo + o2, l2 * 8u, &s.mbar[k & 1]);
+      issue(k + NBUF);
     }
   }
   if ((n & 1) && threadIdx.x == 0) visit(hi - 1, __ldcg(src + hi - 1));
@@ -806,7 +804,7 @@ __device__ void stream_chunk(Smem& s, const double* src, long long lo, long long
 // task reserves the space.
 __device__ __forceinline__ void stage(Smem& s, double x, int list, double* overflow_base,
                                       int dir, unsigned* gcounter) {
-  double* buf = arena(s) + 2 * PIECE + list * STAGE;
+  double* buf = arena(s) + NBUF * PIECE + list * STAGE;
   const int k = atomicAdd(&s.ivals[1 + list], 1);
   if (k < STAGE) {
     buf[k] = x;
@@ -860,7 +858,7 @@ __device__ __noinline__ void run_collect(const Params& p, Smem& s, int v, int c)
   }
   __syncthreads();
   const unsigned long long o1 = s.u64[0], o2 = s.u64[1];
-  const double* st = arena(s) + 2 * PIECE;
+  const double* st = arena(s) + NBUF * PIECE;
   for (int k = threadIdx.x; k < n1; k += NT) cand[o1 + k] = st[k];
   for (int k = threadIdx.x; k < n2s; k += NT) cand2[-(long long)(o2 + k)] = st[STAGE + k];
 }
