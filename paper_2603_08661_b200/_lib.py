@@ -13,7 +13,7 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libigs_b200.so")
+LIB_PATH = os.environ.get("IGS_LIB") or os.path.join(HERE, "libigs_b200.so")  # IGS_LIB: A/B runs
 
 IGS_OK, IGS_ERR_ARGUMENT, IGS_ERR_CUDA, IGS_ERR_WORKSPACE, IGS_ERR_UNSUPPORTED = range(5)
 IGS_F32, IGS_F64 = 0, 1

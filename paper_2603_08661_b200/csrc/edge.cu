@@ -130,7 +130,7 @@ __device__ __forceinline__ double* ring_slot(const Params& p, int v) {
 }
 // the collect pass's two candidate lists: list 1 grows up from here, list 2 down from +npx-1
 __device__ __forceinline__ double* cand_lists(const Params& p, int v) {
-  return ring_slot(p, v) + (p.mode == MODE_FUSED ? 2 * p.npx : 0);
+  return ring_slot(p, v) + (p.mode == MODE_FUSED ? 2 * (p.slot / 3) : 0);
 }
 
 struct __align__(16) Smem {
@@ -205,6 +205,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ double2 ld_cg2(const double* a) {
+  double2 r;
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(a));
+  return r;
 }
 
 __device__ __forceinline__ int clamp_i(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -532,7 +538,7 @@ __device__ void band_nms_finish(const Params& p, Smem& s, int v, int x0, int y_f
   const unsigned n = s.list_n[parity];
   const long long vbase = (long long)v * p.npx;
   double* sval = ring_slot(p, v);
-  unsigned* sidx = reinterpret_cast<unsigned*>(sval + p.npx);
+  unsigned* sidx = reinterpret_cast<unsigned*>(sval + p.slot / 3);
   for (unsigned base = 0; base < n; base += NT) {  // warp-uniform trip count
     const unsigned i = base + threadIdx.x;
     bool surv = false;
@@ -749,9 +755,9 @@ __device__ __forceinline__ int sub_bin(unsigned long long bits) {
 // A C/A task streams its chunk of the thinned map through shared memory in PIECE-sized
 // pieces with TMA bulk copies (two buffers in flight, mbarrier completion), so the task is
 // not limited by register-held loads.  Unaligned views fall back to plain loads.
-constexpr int PIECE = 1536;                     // doubles per piece (12 KB)
+constexpr int PIECE = 1280;                     // doubles per piece (10 KB)
 constexpr int NBUF = 4;                         // pieces in flight
-constexpr int STAGE = 256;                      // staged candidates per list in a C task
+constexpr int STAGE = 512;                      // staged candidates per list in a C task
 static_assert(NBUF * PIECE + 2 * STAGE <= GR * GWP + BR * BWP + QR * MWP / 2,
               "stream buffers fit in g + b + q");
 
@@ -765,6 +771,7 @@ __device__ void stream_chunk(Smem& s, const double* src, long long lo, long long
   const bool aligned = ((((uintptr_t)(src + lo)) & 15) == 0);
   if (!aligned) {
     for (long long i = lo + threadIdx.x; i < hi; i += NT) visit(i, __ldcg(src + i));
+    __syncthreads();  // same exit contract as the bulk path: every visit has completed
     return;
   }
   const long long nfull = n & ~1ll;  // bulk part: a multiple of 16 bytes
@@ -802,16 +809,19 @@ __device__ void stream_chunk(Smem& s, const double* src, long long lo, long long
 // Candidates are bucketed by level-2 bin (returning atomics on the level-2 histogram) and
 // also appended to a flat per-view list: staged in shared memory, then ONE global atomic per
 // task reserves the space.
-__device__ __forceinline__ void stage(Smem& s, double x, int list, double* overflow_base,
+// Stage candidate x of list `list` in shared memory; false (spilled straight to the global
+// list) once STAGE are staged.
+__device__ __forceinline__ bool stage(Smem& s, double x, int list, double* overflow_base,
                                       int dir, unsigned* gcounter) {
   double* buf = arena(s) + NBUF * PIECE + list * STAGE;
   const int k = atomicAdd(&s.ivals[1 + list], 1);
   if (k < STAGE) {
     buf[k] = x;
-  } else {  // rare: more than STAGE candidates in one chunk
-    const unsigned g = atomicAdd(gcounter, 1u);
-    overflow_base[dir * (long long)g] = x;
+    return true;
   }
+  const unsigned g = atomicAdd(gcounter, 1u);  // rare: more than STAGE candidates in a chunk
+  overflow_base[dir * (long long)g] = x;
+  return false;
 }
 
 __device__ __noinline__ void run_collect(const Params& p, Smem& s, int v, int c) {
@@ -839,26 +849,34 @@ __device__ __noinline__ void run_collect(const Params& p, Smem& s, int v, int c)
   double* sla = p.slots + (long long)slot * 2 * NB2 * SLOTS;
   double* slb = sla + NB2 * SLOTS;
   const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, nsrc);
+  auto bucket = [&](double x, int list) {  // level-2 bucket (returning global atomic)
+    const int sb = sub_bin((unsigned long long)__double_as_longlong(x));
+    const unsigned k = atomicAdd(&(list ? h2b : h2a)[sb], 1u);
+    if (k < (unsigned)SLOTS) (list ? slb : sla)[sb * SLOTS + k] = x;
+  };
+  // the scan only stages candidates in shared memory; their global atomics are issued
+  // together afterwards (one round trip per task instead of one per hit)
   stream_chunk(s, src, lo, hi, [&](long long, double x) {
     if (!(x > 0.0)) return;
     const int hb = hist_bin(x);
     if (hb != b1 && hb != b2) return;
     const int list = hb == b1 ? 0 : 1;
-    const int sb = sub_bin((unsigned long long)__double_as_longlong(x));
-    const unsigned k = atomicAdd(&(list ? h2b : h2a)[sb], 1u);
-    if (k < (unsigned)SLOTS) (list ? slb : sla)[sb * SLOTS + k] = x;
-    if (list == 0) stage(s, x, 0, cand, 1, &ctl.cnt1);
-    else stage(s, x, 1, cand2, -1, &ctl.cnt2);
+    if (!stage(s, x, list, list ? cand2 : cand, list ? -1 : 1, list ? &ctl.cnt2 : &ctl.cnt1))
+      bucket(x, list);  // rare: spilled past STAGE, bucketed right away
   });
-  // append the staged lists: one reservation per list
   const int n1 = min(s.ivals[1], STAGE), n2s = min(s.ivals[2], STAGE);
+  const double* st = arena(s) + NBUF * PIECE;
+  for (int k = threadIdx.x; k < n1 + n2s; k += NT) {
+    if (k < n1) bucket(st[k], 0);
+    else bucket(st[STAGE + k - n1], 1);
+  }
+  // append the staged lists: one reservation per list
   if (threadIdx.x == 0) {
     s.u64[0] = n1 ? atomicAdd(&ctl.cnt1, (unsigned)n1) : 0u;
     s.u64[1] = n2s ? atomicAdd(&ctl.cnt2, (unsigned)n2s) : 0u;
   }
   __syncthreads();
   const unsigned long long o1 = s.u64[0], o2 = s.u64[1];
-  const double* st = arena(s) + NBUF * PIECE;
   for (int k = threadIdx.x; k < n1; k += NT) cand[o1 + k] = st[k];
   for (int k = threadIdx.x; k < n2s; k += NT) cand2[-(long long)(o2 + k)] = st[STAGE + k];
 }
@@ -1051,7 +1069,7 @@ __device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, u
   if (p.mode == MODE_FUSED) {
     // survivors only: every other pixel of the thinned map is 0 (0 / 2m = 0) or NaN already
     const double* sval = ring_slot(p, v);
-    const unsigned* sidx = reinterpret_cast<const unsigned*>(sval + p.npx);
+    const unsigned* sidx = reinterpret_cast<const unsigned*>(sval + p.slot / 3);
     const long long n = (long long)__ldcg(&ctl.nsurv);
     const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, n);
     constexpr int U = 4;
@@ -1283,7 +1301,8 @@ Layout layout(long long B, long long npx, bool median) {
   L.slots = off;
   off = align_up(off + sizeof(double) * 2 * NB2 * SLOTS * (size_t)RING, 256);
   L.cand = off;
-  if (median) off = align_up(off + sizeof(double) * 3 * (size_t)npx * (size_t)(B < RING ? B : RING), 256);
+  if (median)
+    off = align_up(off + sizeof(double) * 3 * (size_t)((npx + 1) & ~1ll) * (size_t)(B < RING ? B : RING), 256);
   L.total = off;
   return L;
 }
@@ -1322,7 +1341,7 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   p.hist = (unsigned*)(w + L.hist);
   p.hist2 = (unsigned*)(w + L.hist2);
   p.cand = (double*)(w + L.cand);
-  p.slot = 3 * p.npx;
+  p.slot = 3 * ((p.npx + 1) & ~1ll);  // even: every ring slot starts 16-byte aligned
   p.slots = (double*)(w + L.slots);
   IGS_CUDA_TRY(cudaMemsetAsync(w, 0, L.zero_bytes, stream));  // sched, ctl, hist, hist2
   p.kgray[0] = 0.299;
