@@ -125,12 +125,25 @@ struct Params {
   long long slot;           // doubles per ring slot
 };
 
+// Ring slot of view v (3 * npx_e doubles, npx_e = npx rounded up to even).  Fused mode:
+//   [0, npx_e)               survivor-list values (row segments, see band_nms_decide)
+//   [npx_e, 2 npx_e)         the collect pass's two candidate lists
+//   bytes from 2 npx_e       survivor-list columns (u8, column inside the band)
+//   after those              the row directory: per (image row, band column) a u64
+//                            (list offset << 32 | entries)
+// Median-only mode: the candidate lists at [0, npx).
 __device__ __forceinline__ double* ring_slot(const Params& p, int v) {
   return p.cand + (long long)(v % RING) * p.slot;
 }
-// the collect pass's two candidate lists: list 1 grows up from here, list 2 down from +npx-1
 __device__ __forceinline__ double* cand_lists(const Params& p, int v) {
-  return ring_slot(p, v) + (p.mode == MODE_FUSED ? 2 * (p.slot / 3) : 0);
+  return ring_slot(p, v) + (p.mode == MODE_FUSED ? p.slot / 3 : 0);
+}
+__device__ __forceinline__ unsigned char* surv_cols(const Params& p, int v) {
+  return reinterpret_cast<unsigned char*>(ring_slot(p, v) + 2 * (p.slot / 3));
+}
+__device__ __forceinline__ unsigned long long* row_dir(const Params& p, int v) {
+  const long long ne = p.slot / 3;
+  return reinterpret_cast<unsigned long long*>(ring_slot(p, v) + 2 * ne + (ne + 7) / 8 + 1);
 }
 
 struct __align__(16) Smem {
@@ -139,6 +152,8 @@ struct __align__(16) Smem {
   unsigned q[QR * MWP];     // Sobel cells: (|grad|^2 key << 2) | direction bin
   unsigned short list[SR * TWM];  // compacted NMS survivors / undecided pixels of a sub-step
   unsigned list_n[2];       // list lengths (double-buffered by sub-step parity)
+  unsigned rowl[SR];        // median mode: first s.list entry of each sub-step row
+  unsigned rowg[SR];        // median mode: its position in the view's survivor list
   unsigned hist[NB / 2];    // level-1 counts packed two 16-bit bins per word; radix scratch
   unsigned warp_sums[32];
   int task_kind, task_view, task_idx, flag;
@@ -485,48 +500,64 @@ __device__ __forceinline__ double mag_exact(const Params& p, const Smem& s, int 
 // w + NWARP, lane l columns l + 32 k.  Suppressed pixels store 0 here; survivors and
 // undecided pixels are appended to s.list as (r << 12) | (c << 2) | (undecided prev << 1) |
 // undecided next (warp-aggregated).
-__device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw, int y_first,
-                                int cnt, int parity) {
+__device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw, int cb,
+                                int y_first, int cnt, int parity) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long vbase = (long long)v * p.npx;
+  const unsigned lt = lanemask_lt();
 #pragma unroll
   for (int hh = 0; hh < 2; ++hh) {
     const int r = warp + NWARP * hh;
     if (r >= cnt) continue;
     const unsigned* qrow = s.q + (r + 1) * MWP + 1;  // output column c at qrow[c]
     double* orow = p.out + vbase + (long long)(y_first + r) * p.W + x0;
+    unsigned bal[4], entry[4];
+    bool need[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int c = lane + 32 * k;
       const unsigned qc = qrow[c];
-      unsigned entry = 0;
-      bool need;
       if (p.nms) {
         const int bn = (int)(qc & 3u);
         // prev (dy, dx): bin0 (0,-1), bin1 (-1,-1), bin2 (-1,0), bin3 (-1,+1); next = -prev
         const int po = bn == 0 ? -1 : bn - MWP - 2;  // prev as an offset in s.q cells
         const int kc = (int)(qc >> 2), kp = (int)(qrow[c + po] >> 2), kn = (int)(qrow[c - po] >> 2);
         const int d1 = kc - kp, d2 = kc - kn;
-        const bool sent = kc == (int)KEY_EXACT;
-        const bool u1 = sent || kp == (int)KEY_EXACT || (d1 >= -1 && d1 <= 1 && (kc | kp) != 0);
-        const bool u2 = sent || kn == (int)KEY_EXACT || (d2 >= -1 && d2 <= 1 && (kc | kn) != 0);
+        const bool sent = max(kc, max(kp, kn)) == (int)KEY_EXACT;
+        const bool u1 = sent || ((unsigned)(d1 + 1) <= 2u && (kc | kp) != 0);
+        const bool u2 = sent || ((unsigned)(d2 + 1) <= 2u && (kc | kn) != 0);
         // suppressed for sure: prev decided >= self, or next decided > self
         const bool rej = (!u1 && d1 <= 0) || (!u2 && d2 < 0);
-        need = !rej;
-        entry = ((unsigned)r << 12) | ((unsigned)c << 2) | (u1 ? 2u : 0u) | (u2 ? 1u : 0u);
+        need[k] = !rej;
+        entry[k] = ((unsigned)r << 12) | ((unsigned)c << 2) | (u1 ? 2u : 0u) | (u2 ? 1u : 0u);
       } else {
-        need = (qc >> 2) != 0;
-        entry = ((unsigned)r << 12) | ((unsigned)c << 2);
+        need[k] = (qc >> 2) != 0;
+        entry[k] = ((unsigned)r << 12) | ((unsigned)c << 2);
       }
-      need = need && c < xw;
-      if (!need && c < xw) orow[c] = 0.0;
-      const unsigned bal = __ballot_sync(0xffffffffu, need);
-      if (bal) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&s.list_n[parity], (unsigned)__popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (need) s.list[base + __popc(bal & lanemask_lt())] = (unsigned short)entry;
+      need[k] = need[k] && c < xw;
+      // without the median the map is final here; with it, the apply pass writes whole rows
+      if (!p.median && !need[k] && c < xw) orow[c] = 0.0;
+      bal[k] = __ballot_sync(0xffffffffu, need[k]);
+    }
+    // one contiguous, column-ordered chunk of s.list (and of the view's survivor list) per row
+    const unsigned tot = __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
+    unsigned lbase = 0, gbase = 0;
+    if (lane == 0) {
+      lbase = tot ? atomicAdd(&s.list_n[parity], tot) : 0u;
+      if (p.median) {
+        gbase = tot ? atomicAdd(&p.ctl[v].nsurv, tot) : 0u;
+        s.rowl[r] = lbase;
+        s.rowg[r] = gbase;
+        row_dir(p, v)[(long long)(y_first + r) * p.ncols + cb] =
+            ((unsigned long long)gbase << 32) | tot;
       }
+    }
+    lbase = __shfl_sync(0xffffffffu, lbase, 0);
+    unsigned pre = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (need[k]) s.list[lbase + pre + __popc(bal[k] & lt)] = (unsigned short)entry[k];
+      pre += __popc(bal[k]);
     }
   }
 }
@@ -538,43 +569,29 @@ __device__ void band_nms_finish(const Params& p, Smem& s, int v, int x0, int y_f
   const unsigned n = s.list_n[parity];
   const long long vbase = (long long)v * p.npx;
   double* sval = ring_slot(p, v);
-  unsigned* sidx = reinterpret_cast<unsigned*>(sval + p.slot / 3);
-  for (unsigned base = 0; base < n; base += NT) {  // warp-uniform trip count
-    const unsigned i = base + threadIdx.x;
-    bool surv = false;
-    double outv = 0.0;
-    unsigned pix = 0;
-    if (i < n) {
-      const unsigned e = s.list[i];
-      const int r = (int)(e >> 12), c = (int)((e >> 2) & 0x3ffu);
-      const int y = y_first + r;
-      const double m = mag_exact(p, s, x0, y, r + 1, c + 1);
-      bool keep = true;
-      if (e & 3u) {
-        const int bn = (int)(s.q[(r + 1) * MWP + 1 + c] & 3u);
-        const int dy = bn == 0 ? 0 : -1, dx = bn == 0 ? -1 : bn - 2;
-        if (e & 2u) keep = m > mag_exact(p, s, x0, y + dy, r + 1 + dy, c + 1 + dx);
-        if (keep && (e & 1u)) keep = m >= mag_exact(p, s, x0, y - dy, r + 1 - dy, c + 1 - dx);
-      }
-      outv = keep ? m : 0.0;
-      pix = (unsigned)(y * p.W + x0 + c);
-      // with the median: a positive survivor goes to the view's survivor list (the apply
-      // pass writes its normalised value); everything else is final here (0 / NaN stay)
-      surv = p.median && outv > 0.0;
-      if (surv) hist_add(s, hist_bin(outv));
-      else st_hint(p.out + vbase + pix, outv, pol_mid);
+  unsigned char* scol = surv_cols(p, v);
+  for (unsigned i = threadIdx.x; i < n; i += NT) {
+    const unsigned e = s.list[i];
+    const int r = (int)(e >> 12), c = (int)((e >> 2) & 0x3ffu);
+    const int y = y_first + r;
+    const double m = mag_exact(p, s, x0, y, r + 1, c + 1);
+    bool keep = true;
+    if (e & 3u) {
+      const int bn = (int)(s.q[(r + 1) * MWP + 1 + c] & 3u);
+      const int dy = bn == 0 ? 0 : -1, dx = bn == 0 ? -1 : bn - 2;
+      if (e & 2u) keep = m > mag_exact(p, s, x0, y + dy, r + 1 + dy, c + 1 + dx);
+      if (keep && (e & 1u)) keep = m >= mag_exact(p, s, x0, y - dy, r + 1 - dy, c + 1 - dx);
     }
+    const double outv = keep ? m : 0.0;
     if (p.median) {
-      const unsigned bal = __ballot_sync(0xffffffffu, surv);
-      if (bal) {
-        unsigned at = 0;
-        if ((threadIdx.x & 31) == 0) at = atomicAdd(&p.ctl[v].nsurv, (unsigned)__popc(bal));
-        at = __shfl_sync(0xffffffffu, at, 0) + __popc(bal & lanemask_lt());
-        if (surv) {
-          sval[at] = outv;
-          sidx[at] = pix;
-        }
-      }
+      // the entry's slot in its row segment of the view's survivor list; the apply pass
+      // rebuilds the row from the segment (0 everywhere else)
+      const unsigned at = s.rowg[r] + (i - s.rowl[r]);
+      sval[at] = outv;
+      scol[at] = (unsigned char)c;
+      if (outv > 0.0) hist_add(s, hist_bin(outv));
+    } else {
+      st_hint(p.out + vbase + (long long)y * p.W + x0 + c, outv, pol_mid);
     }
   }
 }
@@ -637,7 +654,7 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
     else band_sobel<false>(p, s, x0, Y + 1, 2, n);
     if (more) shift_rows<double, GWP>(s.g, n, 8);
     __syncthreads();
-    band_nms_decide(p, s, v, x0, xw, Y, n, parity);
+    band_nms_decide(p, s, v, x0, xw, cb, Y, n, parity);
     __syncthreads();
     band_nms_finish(p, s, v, x0, Y, parity, pol_mid);
     parity ^= 1;
@@ -737,8 +754,11 @@ __device__ __noinline__ void find_median_bins(const Params& p, Smem& s, int v) {
       ctl.r2 = r2;
     }
   }
-  if (threadIdx.x == 0)  // fused: C and A tasks walk the survivor list (total entries)
-    ctl.tca = p.mode == MODE_FUSED ? (unsigned)((total + CHUNK - 1) / CHUNK) : (unsigned)p.TC;
+  if (threadIdx.x == 0) {  // C tasks: chunks of the survivor list (fused) or of the input
+    const unsigned long long ns = p.mode == MODE_FUSED ? __ldcg(&ctl.nsurv) : 0ull;
+    ctl.tca = p.mode == MODE_FUSED ? (unsigned)((ns + CHUNK - 1) / CHUNK) : (unsigned)p.TC;
+    if (total == 0) ctl.tca = 0;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1067,26 +1087,85 @@ __device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, u
   const bool plain = isfinite(denom) && denom > 0x1p-1000 && denom < 0x1p+1000;
   double* dst = p.out + (long long)v * p.npx;
   if (p.mode == MODE_FUSED) {
-    // survivors only: every other pixel of the thinned map is 0 (0 / 2m = 0) or NaN already
+    // task c = band c: write the band's final output rows -- zeros (coalesced), then the
+    // normalised survivor-list entries scattered into them (row directory -> row segments).
     const double* sval = ring_slot(p, v);
-    const unsigned* sidx = reinterpret_cast<const unsigned*>(sval + p.slot / 3);
-    const long long n = (long long)__ldcg(&ctl.nsurv);
-    const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, n);
+    const unsigned char* scol = surv_cols(p, v);
+    const unsigned long long* dir = row_dir(p, v);
+    const int cb = c % p.ncols, rb = c / p.ncols;
+    const int x0 = cb * p.tw, xw = min(p.tw, (int)p.W - x0);
+    const int ya = rb * p.band_h, yb = min(ya + p.band_h, (int)p.H);
+    const int rows = yb - ya;  // <= BAND_H
+    unsigned* rg = s.q;                 // row -> list offset
+    unsigned* pre = s.q + BAND_H;       // row -> first flat entry (prefix of the counts)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp < 4) {  // directory + exclusive prefix of the row counts (4 warps x 32 rows)
+      const int r = warp * 32 + lane;
+      unsigned n = 0;
+      if (r < rows) {
+        const unsigned long long d = __ldcg(dir + (long long)(ya + r) * p.ncols + cb);
+        rg[r] = (unsigned)(d >> 32);
+        n = (unsigned)(d & 0xffffffffu);
+      }
+      unsigned inc = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      pre[r] = inc - n;                      // within this warp's 32 rows
+      if (lane == 31) s.warp_sums[warp] = inc;
+    }
+    __syncthreads();
+    if (threadIdx.x < BAND_H) {  // add the preceding warps' totals
+      const int w = threadIdx.x >> 5;
+      unsigned add = 0;
+      for (int k = 0; k < w; ++k) add += s.warp_sums[k];
+      pre[threadIdx.x] += add;
+      if (threadIdx.x == 0) pre[BAND_H] = s.warp_sums[0] + s.warp_sums[1] + s.warp_sums[2] + s.warp_sums[3];
+    }
+    // zero the band's rows (coalesced; the lines stay in L2 for the scatter that follows)
+    for (int r = warp; r < rows; r += NWARP) {
+      double* orow = dst + (long long)(ya + r) * p.W + x0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (lane + 32 * k < xw) orow[lane + 32 * k] = 0.0;
+    }
+    __syncthreads();
+    // scatter the normalised entries, all of the band's loads in flight together
+    const unsigned e1 = pre[BAND_H];
     constexpr int U = 4;
-    for (long long b = lo; b < hi; b += U * NT) {
-      double x[U];
-      unsigned ix[U];
+    for (unsigned e = threadIdx.x; e < e1; e += U * NT) {
+      unsigned at[U];
+      int row[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const long long k = b + u * NT + threadIdx.x;
-        if (k < hi) {
-          x[u] = __ldcg(sval + k);
-          ix[u] = __ldcg(sidx + k);
+        const unsigned ee = e + u * NT;
+        int lo = 0, hi = rows - 1;  // the row holding flat entry ee
+#pragma unroll
+        for (int it = 0; it < 7; ++it) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (lo < hi) {
+            if (pre[mid] <= ee) lo = mid;
+            else hi = mid - 1;
+          }
+        }
+        row[u] = lo;
+        at[u] = ee < e1 ? rg[lo] + (ee - pre[lo]) : 0u;
+      }
+      double val[U];
+      unsigned col[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (e + u * NT < e1) {
+          val[u] = __ldcg(sval + at[u]);
+          col[u] = __ldcg(scol + at[u]);
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (b + u * NT + threadIdx.x < hi) st_hint(dst + ix[u], normalise(x[u], denom, rd, plain), pol_out);
+        if (e + u * NT < e1)
+          dst[(long long)(ya + row[u]) * p.W + x0 + col[u]] = normalise(val[u], denom, rd, plain);
     }
     return;
   }
@@ -1128,7 +1207,8 @@ __device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
       const unsigned v = ld_acquire(&sched[2]);
       if (v >= B || !ld_acquire(&p.ctl[v].select_done)) break;
       const unsigned c = atomicAdd(&p.ctl[v].a_claim, 1u);
-      if (c < __ldcg(&p.ctl[v].tca)) {
+      // fused: one A task per band (it writes the band's final rows); median-only: chunks
+      if (c < (p.mode == MODE_FUSED ? (unsigned)p.TE : (unsigned)p.TC)) {
         kind = TASK_A; view = (int)v; idx = (int)c;
         return;
       }
@@ -1238,7 +1318,8 @@ __global__ void __launch_bounds__(NT, IGS_MINB) edge_persistent_kernel(const __g
     // Claim the next task while this one runs: short tasks claim now; a fused band claims at
     // the start of its last sub-step, so ready C/A work is not held behind a whole band.
     const bool late_claim = kind == TASK_E && p.mode == MODE_FUSED;
-    if (threadIdx.x < 32 && !late_claim) claim_next<CH, F64>(p, s, pol_in);
+    // C / A tasks: the last warp claims (the tasks' first phases use warps 0..3 most)
+    if (threadIdx.x >= NT - 32 && !late_claim) claim_next<CH, F64>(p, s, pol_in);
     if (kind == TASK_E) {
       if (p.mode == MODE_FUSED) run_band<FAST, CH, F64>(p, s, v, idx, pol_in, pol_mid);
       else run_hist_chunk(p, s, v, idx);
