@@ -126,11 +126,9 @@ struct Params {
 };
 
 // Ring slot of view v (3 * npx_e doubles, npx_e = npx rounded up to even).  Fused mode:
-//   [0, npx_e)               survivor-list values (row segments, see band_nms_decide)
+//   [0, npx_e)               survivor-list values (one column-ordered segment per band row)
 //   [npx_e, 2 npx_e)         the collect pass's two candidate lists
-//   bytes from 2 npx_e       survivor-list columns (u8, column inside the band)
-//   after those              the row directory: per (image row, band column) a u64
-//                            (list offset << 32 | entries)
+//   from 2 npx_e             survivor-list pixel indices (u32)
 // Median-only mode: the candidate lists at [0, npx).
 __device__ __forceinline__ double* ring_slot(const Params& p, int v) {
   return p.cand + (long long)(v % RING) * p.slot;
@@ -138,13 +136,10 @@ __device__ __forceinline__ double* ring_slot(const Params& p, int v) {
 __device__ __forceinline__ double* cand_lists(const Params& p, int v) {
   return ring_slot(p, v) + (p.mode == MODE_FUSED ? p.slot / 3 : 0);
 }
-__device__ __forceinline__ unsigned char* surv_cols(const Params& p, int v) {
-  return reinterpret_cast<unsigned char*>(ring_slot(p, v) + 2 * (p.slot / 3));
+__device__ __forceinline__ unsigned* surv_idx(const Params& p, int v) {
+  return reinterpret_cast<unsigned*>(ring_slot(p, v) + 2 * (p.slot / 3));
 }
-__device__ __forceinline__ unsigned long long* row_dir(const Params& p, int v) {
-  const long long ne = p.slot / 3;
-  return reinterpret_cast<unsigned long long*>(ring_slot(p, v) + 2 * ne + (ne + 7) / 8 + 1);
-}
+
 
 struct __align__(16) Smem {
   double g[GR * GWP];       // gray rows of a band sub-step; C/A stream buffers, select scratch
@@ -501,7 +496,7 @@ __device__ __forceinline__ double mag_exact(const Params& p, const Smem& s, int 
 // undecided pixels are appended to s.list as (r << 12) | (c << 2) | (undecided prev << 1) |
 // undecided next (warp-aggregated).
 __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw, int cb,
-                                int y_first, int cnt, int parity) {
+                                int y_first, int cnt, int parity, unsigned long long pol_mid) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long vbase = (long long)v * p.npx;
   const unsigned lt = lanemask_lt();
@@ -535,8 +530,9 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
         entry[k] = ((unsigned)r << 12) | ((unsigned)c << 2);
       }
       need[k] = need[k] && c < xw;
-      // without the median the map is final here; with it, the apply pass writes whole rows
-      if (!p.median && !need[k] && c < xw) orow[c] = 0.0;
+      // every pixel gets a full-line store here (0); survivors are overwritten by finish
+      // (no median) or by the apply pass (median), so no line is ever partially written
+      if ((p.median || !need[k]) && c < xw) st_hint(orow + c, 0.0, pol_mid);
       bal[k] = __ballot_sync(0xffffffffu, need[k]);
     }
     // one contiguous, column-ordered chunk of s.list (and of the view's survivor list) per row
@@ -548,8 +544,6 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
         gbase = tot ? atomicAdd(&p.ctl[v].nsurv, tot) : 0u;
         s.rowl[r] = lbase;
         s.rowg[r] = gbase;
-        row_dir(p, v)[(long long)(y_first + r) * p.ncols + cb] =
-            ((unsigned long long)gbase << 32) | tot;
       }
     }
     lbase = __shfl_sync(0xffffffffu, lbase, 0);
@@ -569,7 +563,7 @@ __device__ void band_nms_finish(const Params& p, Smem& s, int v, int x0, int y_f
   const unsigned n = s.list_n[parity];
   const long long vbase = (long long)v * p.npx;
   double* sval = ring_slot(p, v);
-  unsigned char* scol = surv_cols(p, v);
+  unsigned* sidx = surv_idx(p, v);
   for (unsigned i = threadIdx.x; i < n; i += NT) {
     const unsigned e = s.list[i];
     const int r = (int)(e >> 12), c = (int)((e >> 2) & 0x3ffu);
@@ -588,7 +582,7 @@ __device__ void band_nms_finish(const Params& p, Smem& s, int v, int x0, int y_f
       // rebuilds the row from the segment (0 everywhere else)
       const unsigned at = s.rowg[r] + (i - s.rowl[r]);
       sval[at] = outv;
-      scol[at] = (unsigned char)c;
+      sidx[at] = (unsigned)((long long)y * p.W + x0 + c);
       if (outv > 0.0) hist_add(s, hist_bin(outv));
     } else {
       st_hint(p.out + vbase + (long long)y * p.W + x0 + c, outv, pol_mid);
@@ -654,7 +648,7 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
     else band_sobel<false>(p, s, x0, Y + 1, 2, n);
     if (more) shift_rows<double, GWP>(s.g, n, 8);
     __syncthreads();
-    band_nms_decide(p, s, v, x0, xw, cb, Y, n, parity);
+    band_nms_decide(p, s, v, x0, xw, cb, Y, n, parity, pol_mid);
     __syncthreads();
     band_nms_finish(p, s, v, x0, Y, parity, pol_mid);
     parity ^= 1;
@@ -757,7 +751,6 @@ __device__ __noinline__ void find_median_bins(const Params& p, Smem& s, int v) {
   if (threadIdx.x == 0) {  // C tasks: chunks of the survivor list (fused) or of the input
     const unsigned long long ns = p.mode == MODE_FUSED ? __ldcg(&ctl.nsurv) : 0ull;
     ctl.tca = p.mode == MODE_FUSED ? (unsigned)((ns + CHUNK - 1) / CHUNK) : (unsigned)p.TC;
-    if (total == 0) ctl.tca = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1087,85 +1080,28 @@ __device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, u
   const bool plain = isfinite(denom) && denom > 0x1p-1000 && denom < 0x1p+1000;
   double* dst = p.out + (long long)v * p.npx;
   if (p.mode == MODE_FUSED) {
-    // task c = band c: write the band's final output rows -- zeros (coalesced), then the
-    // normalised survivor-list entries scattered into them (row directory -> row segments).
+    // a chunk of the survivor list: the normalised values overwrite their pixels (the E task
+    // wrote full lines of zeros, so these stores merge into lines still in L2)
     const double* sval = ring_slot(p, v);
-    const unsigned char* scol = surv_cols(p, v);
-    const unsigned long long* dir = row_dir(p, v);
-    const int cb = c % p.ncols, rb = c / p.ncols;
-    const int x0 = cb * p.tw, xw = min(p.tw, (int)p.W - x0);
-    const int ya = rb * p.band_h, yb = min(ya + p.band_h, (int)p.H);
-    const int rows = yb - ya;  // <= BAND_H
-    unsigned* rg = s.q;                 // row -> list offset
-    unsigned* pre = s.q + BAND_H;       // row -> first flat entry (prefix of the counts)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp < 4) {  // directory + exclusive prefix of the row counts (4 warps x 32 rows)
-      const int r = warp * 32 + lane;
-      unsigned n = 0;
-      if (r < rows) {
-        const unsigned long long d = __ldcg(dir + (long long)(ya + r) * p.ncols + cb);
-        rg[r] = (unsigned)(d >> 32);
-        n = (unsigned)(d & 0xffffffffu);
-      }
-      unsigned inc = n;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      pre[r] = inc - n;                      // within this warp's 32 rows
-      if (lane == 31) s.warp_sums[warp] = inc;
-    }
-    __syncthreads();
-    if (threadIdx.x < BAND_H) {  // add the preceding warps' totals
-      const int w = threadIdx.x >> 5;
-      unsigned add = 0;
-      for (int k = 0; k < w; ++k) add += s.warp_sums[k];
-      pre[threadIdx.x] += add;
-      if (threadIdx.x == 0) pre[BAND_H] = s.warp_sums[0] + s.warp_sums[1] + s.warp_sums[2] + s.warp_sums[3];
-    }
-    // zero the band's rows (coalesced; the lines stay in L2 for the scatter that follows)
-    for (int r = warp; r < rows; r += NWARP) {
-      double* orow = dst + (long long)(ya + r) * p.W + x0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (lane + 32 * k < xw) orow[lane + 32 * k] = 0.0;
-    }
-    __syncthreads();
-    // scatter the normalised entries, all of the band's loads in flight together
-    const unsigned e1 = pre[BAND_H];
+    const unsigned* sidx = surv_idx(p, v);
+    const long long n = (long long)__ldcg(&ctl.nsurv);
+    const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, n);
     constexpr int U = 4;
-    for (unsigned e = threadIdx.x; e < e1; e += U * NT) {
-      unsigned at[U];
-      int row[U];
+    for (long long b = lo; b < hi; b += U * NT) {
+      double x[U];
+      unsigned ix[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const unsigned ee = e + u * NT;
-        int lo = 0, hi = rows - 1;  // the row holding flat entry ee
-#pragma unroll
-        for (int it = 0; it < 7; ++it) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (lo < hi) {
-            if (pre[mid] <= ee) lo = mid;
-            else hi = mid - 1;
-          }
-        }
-        row[u] = lo;
-        at[u] = ee < e1 ? rg[lo] + (ee - pre[lo]) : 0u;
-      }
-      double val[U];
-      unsigned col[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (e + u * NT < e1) {
-          val[u] = __ldcg(sval + at[u]);
-          col[u] = __ldcg(scol + at[u]);
+        const long long k = b + u * NT + threadIdx.x;
+        if (k < hi) {
+          x[u] = __ldcg(sval + k);
+          ix[u] = __ldcg(sidx + k);
         }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (e + u * NT < e1)
-          dst[(long long)(ya + row[u]) * p.W + x0 + col[u]] = normalise(val[u], denom, rd, plain);
+        if (b + u * NT + threadIdx.x < hi && x[u] != 0.0)
+          st_hint(dst + ix[u], normalise(x[u], denom, rd, plain), pol_out);
     }
     return;
   }
@@ -1207,8 +1143,7 @@ __device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
       const unsigned v = ld_acquire(&sched[2]);
       if (v >= B || !ld_acquire(&p.ctl[v].select_done)) break;
       const unsigned c = atomicAdd(&p.ctl[v].a_claim, 1u);
-      // fused: one A task per band (it writes the band's final rows); median-only: chunks
-      if (c < (p.mode == MODE_FUSED ? (unsigned)p.TE : (unsigned)p.TC)) {
+      if (c < (p.mode == MODE_FUSED ? __ldcg(&p.ctl[v].tca) : (unsigned)p.TC)) {
         kind = TASK_A; view = (int)v; idx = (int)c;
         return;
       }
