@@ -306,6 +306,8 @@ def run_ours(args, world, rank, local):
     }
     if not args.no_e2e:
         line["e2e"] = e2e_edge(args, world, dev)
+    if not args.no_uhd:
+        line["edge_uhd"] = bench_uhd(args, world, dev, peak)
     if not args.no_las:
         line["las"] = bench_las(args, world, dev, peak, peak_src)
         line["densify_sharded"] = bench_densify_sharded(args, world, rank, dev)
@@ -429,6 +431,41 @@ def bench_las(args, world, dev, peak, peak_src):
 
 
 DENSIFY_N = 6_000_000
+UHD_VIEWS = 128
+
+
+def bench_uhd(args, world, dev, peak):
+    """BASELINE.json configs[4]: 3840x2160 views, 128 per GPU (1024 over 8 GPUs); the same
+    fused launch as the headline, weak scaling, max-over-ranks device time."""
+    import torch
+
+    import paper_2603_08661_b200 as igs
+    from paper_2603_08661_b200.synth import UHD_H, UHD_W, synth_views_torch
+    views = synth_views_torch(UHD_VIEWS, UHD_H, UHD_W, seed=5000, device=dev, distinct=4)
+    out = torch.empty((UHD_VIEWS, UHD_H, UHD_W), dtype=torch.float64, device=dev)
+    for _ in range(2):
+        igs.importance_batch(views, out=out)
+    steps = max(2, min(args.steps, 5))
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        igs.importance_batch(views, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    px = UHD_VIEWS * UHD_H * UHD_W
+    achieved = px * BYTES_PER_PX_F64 / (ms * 1e-3) / 1e9
+    del views, out
+    torch.cuda.empty_cache()
+    return {"metric": "edge-map MPix/s", "value": round(world * px / (ms * 1e-3) / 1e6, 3),
+            "unit": "MPix/s", "ms_per_step": round(ms, 3), "steps": steps, "scaling": "weak",
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4)},
+            "config": {"workload": f"{UHD_VIEWS} x 3840x2160 RGB f64 views per GPU "
+                                   "(BASELINE.json configs[4]: 1024 over 8 GPUs)",
+                       "l2": "25 GB of input per GPU >> L2"}}
 
 
 def bench_densify_sharded(args, world, rank, dev):
@@ -494,6 +531,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-las", action="store_true")
+    ap.add_argument("--no-uhd", action="store_true")
     args = ap.parse_args()
     args.steps_given = args.steps is not None
     if args.steps is None:

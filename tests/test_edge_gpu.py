@@ -238,3 +238,13 @@ def test_sample_scores_large_batched_and_errors():
     with pytest.raises(IndexError):
         b.sample_scores(maps, pos[:4], view=[0, 1, 2, 3])
     assert b.sample_scores(maps[0], np.zeros((0, 2))).shape == (0,)
+
+
+def test_uhd_view_bit_exact():
+    """BASELINE.json configs[4] shape: a 3840x2160 view (31 band columns x 34 band rows)."""
+    b = B()
+    from paper_2603_08661_b200.synth import UHD_H, UHD_W, synth_view
+    img = synth_view(UHD_H, UHD_W, 4242)
+    got = b.importance_batch(torch.from_numpy(img[None]).cuda()).cpu().numpy()[0]
+    want = OE.importance_pipeline(img)
+    assert np.flatnonzero(got != want).size == 0
