@@ -500,59 +500,73 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long vbase = (long long)v * p.npx;
   const unsigned lt = lanemask_lt();
+  unsigned bal[2][4];
+  unsigned short entry[2][4];
+  unsigned tot[2] = {0u, 0u};
 #pragma unroll
   for (int hh = 0; hh < 2; ++hh) {
     const int r = warp + NWARP * hh;
-    if (r >= cnt) continue;
+    const bool row_ok = r < cnt;  // warp-uniform
     const unsigned* qrow = s.q + (r + 1) * MWP + 1;  // output column c at qrow[c]
     double* orow = p.out + vbase + (long long)(y_first + r) * p.W + x0;
-    unsigned bal[4], entry[4];
-    bool need[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int c = lane + 32 * k;
-      const unsigned qc = qrow[c];
-      if (p.nms) {
-        const int bn = (int)(qc & 3u);
-        // prev (dy, dx): bin0 (0,-1), bin1 (-1,-1), bin2 (-1,0), bin3 (-1,+1); next = -prev
-        const int po = bn == 0 ? -1 : bn - MWP - 2;  // prev as an offset in s.q cells
-        const int kc = (int)(qc >> 2), kp = (int)(qrow[c + po] >> 2), kn = (int)(qrow[c - po] >> 2);
-        const int d1 = kc - kp, d2 = kc - kn;
-        const bool sent = max(kc, max(kp, kn)) == (int)KEY_EXACT;
-        const bool u1 = sent || ((unsigned)(d1 + 1) <= 2u && (kc | kp) != 0);
-        const bool u2 = sent || ((unsigned)(d2 + 1) <= 2u && (kc | kn) != 0);
-        // suppressed for sure: prev decided >= self, or next decided > self
-        const bool rej = (!u1 && d1 <= 0) || (!u2 && d2 < 0);
-        need[k] = !rej;
-        entry[k] = ((unsigned)r << 12) | ((unsigned)c << 2) | (u1 ? 2u : 0u) | (u2 ? 1u : 0u);
-      } else {
-        need[k] = (qc >> 2) != 0;
-        entry[k] = ((unsigned)r << 12) | ((unsigned)c << 2);
+      bool need = false;
+      entry[hh][k] = 0;
+      if (row_ok) {
+        const unsigned qc = qrow[c];
+        if (p.nms) {
+          const int bn = (int)(qc & 3u);
+          // prev (dy, dx): bin0 (0,-1), bin1 (-1,-1), bin2 (-1,0), bin3 (-1,+1); next = -prev
+          const int po = bn == 0 ? -1 : bn - MWP - 2;  // prev as an offset in s.q cells
+          const int kc = (int)(qc >> 2), kp = (int)(qrow[c + po] >> 2), kn = (int)(qrow[c - po] >> 2);
+          const int d1 = kc - kp, d2 = kc - kn;
+          const bool sent = max(kc, max(kp, kn)) == (int)KEY_EXACT;
+          const bool u1 = sent || ((unsigned)(d1 + 1) <= 2u && (kc | kp) != 0);
+          const bool u2 = sent || ((unsigned)(d2 + 1) <= 2u && (kc | kn) != 0);
+          // suppressed for sure: prev decided >= self, or next decided > self
+          need = !((!u1 && d1 <= 0) || (!u2 && d2 < 0));
+          entry[hh][k] = (unsigned short)(((unsigned)r << 12) | ((unsigned)c << 2) | (u1 ? 2u : 0u) |
+                                          (u2 ? 1u : 0u));
+        } else {
+          need = (qc >> 2) != 0;
+          entry[hh][k] = (unsigned short)(((unsigned)r << 12) | ((unsigned)c << 2));
+        }
+        const bool in = c < xw;
+        need = need && in;
+        // every pixel gets a full-line store here (0); survivors are overwritten by finish
+        // (no median) or by the apply pass (median), so no line is ever partially written
+        if ((p.median || !need) && in) st_hint(orow + c, 0.0, pol_mid);
       }
-      need[k] = need[k] && c < xw;
-      // every pixel gets a full-line store here (0); survivors are overwritten by finish
-      // (no median) or by the apply pass (median), so no line is ever partially written
-      if ((p.median || !need[k]) && c < xw) st_hint(orow + c, 0.0, pol_mid);
-      bal[k] = __ballot_sync(0xffffffffu, need[k]);
+      bal[hh][k] = __ballot_sync(0xffffffffu, need);
+      tot[hh] += __popc(bal[hh][k]);
     }
-    // one contiguous, column-ordered chunk of s.list (and of the view's survivor list) per row
-    const unsigned tot = __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
-    unsigned lbase = 0, gbase = 0;
-    if (lane == 0) {
-      lbase = tot ? atomicAdd(&s.list_n[parity], tot) : 0u;
-      if (p.median) {
-        gbase = tot ? atomicAdd(&p.ctl[v].nsurv, tot) : 0u;
-        s.rowl[r] = lbase;
-        s.rowg[r] = gbase;
-      }
+  }
+  // one shared-list chunk per row (column order) and ONE survivor-list reservation per warp
+  unsigned lbase0 = 0, lbase1 = 0, gbase = 0;
+  if (lane == 0) {
+    if (tot[0] + tot[1]) {
+      lbase0 = atomicAdd(&s.list_n[parity], tot[0] + tot[1]);
+      if (p.median) gbase = atomicAdd(&p.ctl[v].nsurv, tot[0] + tot[1]);
     }
-    lbase = __shfl_sync(0xffffffffu, lbase, 0);
-    unsigned pre = 0;
+    lbase1 = lbase0 + tot[0];
+  }
+  lbase0 = __shfl_sync(0xffffffffu, lbase0, 0);
+  lbase1 = __shfl_sync(0xffffffffu, lbase1, 0);
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    unsigned pre = hh ? lbase1 : lbase0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (need[k]) s.list[lbase + pre + __popc(bal[k] & lt)] = (unsigned short)entry[k];
-      pre += __popc(bal[k]);
+      if ((bal[hh][k] >> lane) & 1u) s.list[pre + __popc(bal[hh][k] & lt)] = entry[hh][k];
+      pre += __popc(bal[hh][k]);
     }
+  }
+  if (lane == 0 && p.median) {  // row r's entries: list [rowl, ...) -> survivor list [rowg, ...)
+    const int r0 = warp, r1 = warp + NWARP;
+    if (r0 < cnt) { s.rowl[r0] = lbase0; s.rowg[r0] = gbase; }
+    if (r1 < cnt) { s.rowl[r1] = lbase1; s.rowg[r1] = gbase + tot[0]; }
   }
 }
 
