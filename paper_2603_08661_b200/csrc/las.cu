@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(1024) las_scan_kernel(const unsigned* tile_cnt
 template <int Q4>
 __device__ __forceinline__ void clone_rows(float* sh, const long long* src_idx, unsigned n,
                                            unsigned long long slot0) {
-  constexpr int U = 4;
+  constexpr int U = 8;
   const float4* src = reinterpret_cast<const float4*>(sh);
   float4* dstp = reinterpret_cast<float4*>(sh);
   const unsigned total = n * Q4;
