@@ -119,6 +119,12 @@ int igs_select_candidates(const double* grad_sum, int64_t accum_count, const dou
                           int64_t take_cap, uint8_t* mask, int64_t* counts,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* Trainer-side statistics (splat2d.py:393-394 + densify_controller.py:54-63): grad_sum[i] +=
+ * hypot(grads[2i], grads[2i+1]) in float64 (glibc hypot, as np.hypot); grads (n, 2) of dtype
+ * IGS_F32 / IGS_F64.  The caller increments the accumulation count. */
+int igs_accumulate_grad_norms(double* grad_sum, const void* grads, int dtype, int64_t n,
+                              void* stream);
+
 /* ---- sharded selection (multi-GPU) ---------------------- *
  * The same result as igs_select_candidates over the concatenation of every rank's
  * contiguous shard (densify_controller.py:80-106 on the global arrays), split into the

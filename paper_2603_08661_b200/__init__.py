@@ -10,7 +10,8 @@ bound with ctypes.  There is no CPU fallback.
 
 from .core import Scene3
 from .densify_controller import (EVENT_CSV_HEADER, DensifyEvent, DensifyStats,
-                                 accumulate_grads, densify_step, select_candidates)
+                                 accumulate_grads, accumulate_position_grads, densify_step,
+                                 select_candidates)
 from .edge_pipeline import (GradientField, blur_kernel_5x5, gaussian_blur_5x5,
                             importance_batch, importance_pipeline, median_normalize,
                             nms_thin, sample_scores, sobel_gradients, to_grayscale)

@@ -44,6 +44,7 @@ SIGNATURES = {
     "igs_select_workspace_bytes": (_int, [_i64, _szp]),
     "igs_select_candidates": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _i64, _vp, _vp, _vp,
                                      _sz, _vp]),
+    "igs_accumulate_grad_norms": (_int, [_vp, _vp, _int, _i64, _vp]),
     "igs_select_shard_workspace_bytes": (_int, [_i64, _szp]),
     "igs_select_shard_keys": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _vp, _vp, _sz, _vp]),
     "igs_select_shard_resolve": (_int, [_vp, _int, _i64, _vp, _sz, _vp, _vp]),

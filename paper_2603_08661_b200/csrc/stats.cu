@@ -1,0 +1,60 @@
+// Densification statistics on sm_100a: fold one iteration's positional gradients into the
+// per-primitive running sums, fused with their norm.
+//
+// Replaces the trainer's `accumulate_grads(stats, np.hypot(g[:, 0], g[:, 1]))`
+// (/root/reference/pkg/src/splitkit/splat2d.py:393-394 with densify_controller.py:54-63):
+// grad_sum[i] += hypot(gx, gy) with glibc's hypot / hypotf for float64 / float32 gradients
+// (bit-exact with np.hypot on the same dtype) and one rounded float64 add, so the statistics
+// the selection reads never leave the device.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "igs_common.cuh"
+
+namespace igs {
+namespace stats {
+
+constexpr int NT = 256;
+
+// np.hypot on float32 pairs is glibc's hypotf: the double sqrt of the double sum of squares,
+// rounded to float (inf wins over NaN).
+__device__ __forceinline__ float hypotf_glibc(float x, float y) {
+  if (isinf(x) || isinf(y)) return __int_as_float(0x7f800000);
+  const double dx = x, dy = y;
+  return (float)sqrt(dx * dx + dy * dy);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) accumulate_kernel(double* __restrict__ grad_sum,
+                                                        const T* __restrict__ g, long long n) {
+  const long long i = (long long)blockIdx.x * NT + threadIdx.x;
+  if (i >= n) return;
+  double h;
+  if (sizeof(T) == 8) h = hypot_glibc((double)g[2 * i], (double)g[2 * i + 1]);
+  else h = (double)hypotf_glibc((float)g[2 * i], (float)g[2 * i + 1]);
+  grad_sum[i] = grad_sum[i] + h;
+}
+
+}  // namespace stats
+}  // namespace igs
+
+using namespace igs;
+
+extern "C" {
+
+int igs_accumulate_grad_norms(double* grad_sum, const void* grads, int dtype, int64_t n,
+                              void* stream) {
+  if (n < 0 || (dtype != IGS_F32 && dtype != IGS_F64)) return IGS_ERR_ARGUMENT;
+  if (n == 0) return IGS_OK;
+  if (!grad_sum || !grads) return IGS_ERR_ARGUMENT;
+  const unsigned blocks = (unsigned)((n + stats::NT - 1) / stats::NT);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == IGS_F64)
+    stats::accumulate_kernel<double><<<blocks, stats::NT, 0, st>>>(grad_sum, (const double*)grads, n);
+  else
+    stats::accumulate_kernel<float><<<blocks, stats::NT, 0, st>>>(grad_sum, (const float*)grads, n);
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
+}  // extern "C"

@@ -72,6 +72,25 @@ def accumulate_grads(stats: DensifyStats, step_grad_norms) -> DensifyStats:
     return stats
 
 
+def accumulate_position_grads(stats: DensifyStats, grad_xy) -> DensifyStats:
+    """accumulate_grads(stats, np.hypot(g[:, 0], g[:, 1])) fused on the device
+    (splat2d.py:393-394): one kernel adds glibc-exact float64 hypot of each primitive's (x, y)
+    positional gradient to its running sum."""
+    g = grad_xy if isinstance(grad_xy, torch.Tensor) else torch.as_tensor(np.asarray(grad_xy))
+    if g.dtype not in (torch.float32, torch.float64):
+        g = g.to(torch.float64)
+    g = g.to(stats._device).contiguous()
+    if g.ndim != 2 or g.shape[1] != 2 or g.shape[0] != len(stats):
+        raise ValueError(f"positional gradients {tuple(g.shape)} do not match stats length "
+                         f"{len(stats)} (need (N, 2))")
+    L = _lib.lib()
+    _lib.check(L.igs_accumulate_grad_norms(stats._grad_sum.data_ptr(), g.data_ptr(),
+                                           _lib.IGS_F64 if g.dtype == torch.float64 else _lib.IGS_F32,
+                                           len(stats), _lib.stream_handle()), "accumulate_grads")
+    stats._accum_count += 1
+    return stats
+
+
 def _take_cap(cfg: DensifyConfig, count: int, headroom: int) -> int:
     """min(headroom, max(ceil(growth_cap*count - 1e-9), 0)) (densify_controller.py:99-100)."""
     cap = math.ceil(cfg.growth_cap * count - 1e-9)

@@ -122,3 +122,22 @@ def test_densify_step_guards():
     b.accumulate_grads(st, np.ones(4))
     ev = b.densify_step(s, st, b.DensifyConfig(budget=4, grad_threshold=0.0, growth_cap=1.0), 2000)
     assert ev.split == 0 and s.count == 4 and ev.eligible == 4
+
+
+def test_accumulate_position_grads_matches_numpy_hypot():
+    """splat2d.py:393-394: accumulate_grads(stats, np.hypot(g[:, 0], g[:, 1])), fused."""
+    b = B()
+    rng = np.random.default_rng(31)
+    n = 100_003
+    st = b.DensifyStats(n)
+    want = np.zeros(n)
+    for it, dt in enumerate((np.float64, np.float32, np.float64)):
+        g = (rng.standard_normal((n, 2)) * np.exp(rng.uniform(-30, 5, (n, 1)))).astype(dt)
+        g[:5] = [[0.0, 0.0], [-0.0, 3.0], [np.inf, 1.0], [1e-310, 1e-310], [3e300, 4e300]]
+        b.accumulate_position_grads(st, g)
+        with np.errstate(all="ignore"):
+            want = want + np.hypot(g[:, 0], g[:, 1]).astype(np.float64)
+        assert st._accum_count == it + 1
+    np.testing.assert_array_equal(st._grad_sum.cpu().numpy(), want)
+    with pytest.raises(ValueError):
+        b.accumulate_position_grads(st, np.zeros((n, 3)))
