@@ -785,6 +785,9 @@ __device__ __forceinline__ int sub_bin(unsigned long long bits) {
 constexpr int PIECE = 1280;                     // doubles per piece (10 KB)
 constexpr int NBUF = 4;                         // pieces in flight
 constexpr int STAGE = 512;                      // staged candidates per list in a C task
+constexpr int APIECE = 1024;                    // survivor entries per apply piece (12 KB)
+static_assert(NBUF * APIECE * 12 <= (GR * GWP + BR * BWP) * 8 + QR * MWP * 4, "apply pieces fit in g + b + q");
+static_assert(CHUNK % APIECE == 0 && APIECE % 4 == 0, "apply pieces tile a chunk");
 static_assert(NBUF * PIECE + 2 * STAGE <= GR * GWP + BR * BWP + QR * MWP / 2,
               "stream buffers fit in g + b + q");
 
@@ -1096,26 +1099,58 @@ __device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, u
   if (p.mode == MODE_FUSED) {
     // a chunk of the survivor list: the normalised values overwrite their pixels (the E task
     // wrote full lines of zeros, so these stores merge into lines still in L2)
+    // values and pixel indices arrive by TMA bulk copies, NBUF pieces of APIECE entries in
+    // flight (the list is 16-byte aligned at every chunk start; a piece's copy may run past the
+    // chunk end inside the list allocation -- those entries are not visited)
     const double* sval = ring_slot(p, v);
     const unsigned* sidx = surv_idx(p, v);
     const long long n = (long long)__ldcg(&ctl.nsurv);
     const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, n);
-    constexpr int U = 4;
-    for (long long b = lo; b < hi; b += U * NT) {
-      double x[U];
-      unsigned ix[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long k = b + u * NT + threadIdx.x;
-        if (k < hi) {
-          x[u] = __ldcg(sval + k);
-          ix[u] = __ldcg(sidx + k);
-        }
+    const int npieces = (int)((hi - lo + APIECE - 1) / APIECE);
+    double* vbuf = arena(s);
+    unsigned* ibuf = reinterpret_cast<unsigned*>(arena(s) + NBUF * APIECE);
+    auto issue = [&](int k) {
+      const long long off = lo + (long long)k * APIECE;
+      const unsigned len = (unsigned)min((long long)APIECE, hi - off);
+      const unsigned len4 = (len + 3u) & ~3u;  // 16-byte multiple for the index copy
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_u32(&s.mbar[k % NBUF])),
+                   "r"(len4 * 12u)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(smem_u32(vbuf + (k % NBUF) * APIECE)),
+          "l"(sval + off), "r"(len4 * 8u), "r"(smem_u32(&s.mbar[k % NBUF]))
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(smem_u32(ibuf + (k % NBUF) * APIECE)),
+          "l"(sidx + off), "r"(len4 * 4u), "r"(smem_u32(&s.mbar[k % NBUF]))
+          : "memory");
+    };
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < NBUF; ++k) mbar_init(&s.mbar[k]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      fence_proxy_async();
+      for (int k = 0; k < NBUF && k < npieces; ++k) issue(k);
+    }
+    __syncthreads();
+    for (int k = 0; k < npieces; ++k) {
+      mbar_wait(&s.mbar[k % NBUF], (unsigned)((k / NBUF) & 1));
+      const long long off = lo + (long long)k * APIECE;
+      const int len = (int)min((long long)APIECE, hi - off);
+      const double* vb = vbuf + (k % NBUF) * APIECE;
+      const unsigned* ib = ibuf + (k % NBUF) * APIECE;
+      for (int i = threadIdx.x; i < len; i += NT) {
+        const double x = vb[i];
+        if (x != 0.0) st_hint(dst + ib[i], normalise(x, denom, rd, plain), pol_out);
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (b + u * NT + threadIdx.x < hi && x[u] != 0.0)
-          st_hint(dst + ix[u], normalise(x[u], denom, rd, plain), pol_out);
+      __syncthreads();
+      if (threadIdx.x == 0 && k + NBUF < npieces) {
+        fence_proxy_async();
+        issue(k + NBUF);
+      }
     }
     return;
   }
