@@ -144,7 +144,9 @@ __device__ __forceinline__ unsigned* surv_idx(const Params& p, int v) {
 struct __align__(16) Smem {
   double g[GR * GWP];       // gray rows of a band sub-step; C/A stream buffers, select scratch
   double b[BR * BWP];       // blurred rows (contiguous with g)
-  unsigned q[QR * MWP];     // Sobel cells: (|grad|^2 key << 2) | direction bin
+  unsigned q[(QR + 1) * MWP];  // Sobel cells: (|grad|^2 key << 2) | direction bin; one pad
+                               // row: the NMS neighbour reads of the unused columns past the
+                               // band stay inside the array
   unsigned short list[SR * TWM];  // compacted NMS survivors / undecided pixels of a sub-step
   unsigned list_n[2];       // list lengths (double-buffered by sub-step parity)
   unsigned rowl[SR];        // median mode: first s.list entry of each sub-step row
