@@ -13,7 +13,8 @@
 //              their top 11 bits.
 //   passes 1-5 radix select of the take-th smallest key, 11/11/11/11/9 bits
 //              (grid barrier after each histogram; every block resolves the
-//              digit redundantly from the merged histogram).
+//              digit redundantly from the merged histogram), stopping early once
+//              the take-th key is the last of its bucket (whole bucket taken).
 //   final      key < T selected; ties key == T selected in ascending index
 //              order up to the remaining budget, using an exclusive scan of
 //              per-block tie counts (bit-exact with the stable argsort).
@@ -70,12 +71,14 @@ struct Smem {
   unsigned h[NBK];
   unsigned warp_sums[32];
   unsigned long long u64[4];
-  unsigned u32[4];
+  unsigned u32[4];  // [0] digit, [1] tie scratch, [2] bucket count
 };
 
 // Every block: find the digit of rank `rank` in the merged histogram of pass p.
+// count: how many keys fall in the chosen digit's bucket.
 __device__ void resolve_digit(const Params& P, Smem& s, int p, unsigned long long& prefix,
-                              unsigned long long& pmask, unsigned long long& rank) {
+                              unsigned long long& pmask, unsigned long long& rank,
+                              unsigned& count) {
   const unsigned* gh = P.hist + p * NBK;
   constexpr int PER = NBK / NT;
   unsigned loc[PER], sum = 0;
@@ -91,6 +94,7 @@ __device__ void resolve_digit(const Params& P, Smem& s, int p, unsigned long lon
   for (int k = 0; k < PER; ++k) {
     if (loc[k] && rank >= cum && rank < cum + loc[k]) {
       s.u32[0] = threadIdx.x * PER + k;
+      s.u32[2] = loc[k];
       s.u64[0] = rank - cum;
     }
     cum += loc[k];
@@ -100,6 +104,7 @@ __device__ void resolve_digit(const Params& P, Smem& s, int p, unsigned long lon
   prefix |= (unsigned long long)s.u32[0] << sh;
   pmask |= (unsigned long long)pass_mask(p) << sh;
   rank = s.u64[0];
+  count = s.u32[2];
   __syncthreads();
 }
 
@@ -148,8 +153,12 @@ __global__ void __launch_bounds__(NT) select_kernel(Params P) {
     return;
   }
   unsigned long long prefix = 0, pmask = 0, rank = take - 1;
-  resolve_digit(P, s, 0, prefix, pmask, rank);
-  for (int p = 1; p < PASSES; ++p) {
+  unsigned count = 0;
+  resolve_digit(P, s, 0, prefix, pmask, rank, count);
+  // Early exit (uniform over the grid): once the take-th key is the LAST of its bucket, the
+  // whole bucket is selected and no tie needs ranking -- the mask is (key & pmask) <= prefix.
+  bool whole = rank + 1 == count;
+  for (int p = 1; p < PASSES && !whole; ++p) {
     for (int i = threadIdx.x; i < NBK; i += NT) s.h[i] = 0;
     __syncthreads();
     const int sh = pass_shift(p);
@@ -162,7 +171,15 @@ __global__ void __launch_bounds__(NT) select_kernel(Params P) {
     for (int i = threadIdx.x; i < NBK; i += NT)
       if (s.h[i]) atomicAdd(&P.hist[p * NBK + i], s.h[i]);
     grid.sync();
-    resolve_digit(P, s, p, prefix, pmask, rank);
+    resolve_digit(P, s, p, prefix, pmask, rank, count);
+    whole = rank + 1 == count;
+  }
+  if (whole) {
+    for (long long i = lo + threadIdx.x; i < hi; i += NT) {
+      const unsigned long long k = __ldcg(&P.keys[i]);
+      P.mask[i] = k != kIneligible && (k & pmask) <= prefix;
+    }
+    return;
   }
   const unsigned long long T = prefix;
   const unsigned long long need_ties = rank + 1;  // ties of T inside the top `take`
