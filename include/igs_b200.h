@@ -104,6 +104,11 @@ int igs_sample_scores(const double* maps, int64_t batch, int64_t height, int64_t
  * receives the number of records the previous launches produced. */
 int igs_debug_edge_trace(void* buf, int64_t capacity, int64_t* written);
 
+/* Debug: per-phase nanoseconds of the fused kernel's band sub-steps, summed over blocks
+ * (gray, blur, Sobel, NMS decide, NMS finish), in a library built with -DIGS_PHASE_PROF;
+ * IGS_ERR_UNSUPPORTED otherwise.  reset != 0 clears the counters after reading. */
+int igs_debug_edge_phases(uint64_t* out8, int reset);
+
 /* ---- budgeted candidate selection (densify_controller.py:66-106) -------- */
 
 int igs_select_workspace_bytes(int64_t n, size_t* bytes);

@@ -41,6 +41,7 @@ SIGNATURES = {
     "igs_median_normalize": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "igs_sample_scores": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp]),
     "igs_debug_edge_trace": (_int, [_vp, _i64, C.POINTER(C.c_int64)]),
+    "igs_debug_edge_phases": (_int, [_vp, _int]),
     "igs_select_workspace_bytes": (_int, [_i64, _szp]),
     "igs_select_candidates": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _i64, _vp, _vp, _vp,
                                      _sz, _vp]),

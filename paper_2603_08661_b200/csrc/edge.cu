@@ -52,8 +52,8 @@ constexpr int SH = SR / 2;                   // rows per blur / Sobel strip (two
 #define IGS_MINB 3
 #endif
 constexpr int TWM = 124;                     // max output columns per band
-constexpr int BAND_H = 128;                  // max rows per band (tuning override)
-constexpr int BAND_H_DEFAULT = 64;           // rows per band
+constexpr int BAND_H = 256;                  // max rows per band (tuning override)
+constexpr int BAND_H_DEFAULT = 128;          // rows per band
 constexpr int GWP = TWM + 8, BWP = 128, MWP = 128;  // row pitches (cells); the blur /
                                                     // Sobel lanes cover 128 columns
 constexpr int GR = SR + 8, BR = SR + 4, QR = SR + 2;        // rows per sub-step + context
@@ -626,6 +626,23 @@ __device__ __forceinline__ void shift_rows(E* a, int from, int n, int wbase = 0)
   }
 }
 
+#ifdef IGS_PHASE_PROF
+__device__ unsigned long long g_phase_ns[8];
+#define PHASE_MARK(i)                                                             \
+  do {                                                                            \
+    if (threadIdx.x == 0) {                                                       \
+      unsigned long long _t;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                      \
+      atomicAdd(&g_phase_ns[i], _t - t_prev);                                     \
+      t_prev = _t;                                                                \
+    }                                                                             \
+  } while (0)
+#else
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
+
 template <bool FAST, int CH, bool F64>
 __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long long pol_in,
                          unsigned long long pol_mid) {
@@ -633,6 +650,10 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
   const int cb = t % p.ncols, rb = t / p.ncols;
   const int x0 = cb * p.tw, xw = min(p.tw, W - x0);
   const int ya = rb * p.band_h, yb = min(ya + p.band_h, H);
+#ifdef IGS_PHASE_PROF
+  unsigned long long t_prev = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev));
+#endif
   // prologue: gray rows [ya-4, ya+4) -> s.g rows 0..7; blurred [ya-2, ya+2) -> s.b rows 0..3;
   // Sobel rows [ya-1, ya+1) -> s.q rows 0..1
   if (threadIdx.x == 0) s.list_n[0] = 0;
@@ -643,6 +664,7 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
   if (p.nms) band_sobel<true>(p, s, x0, ya - 1, 0, 2);
   else band_sobel<false>(p, s, x0, ya - 1, 0, 2);
   int parity = 0;
+  PHASE_MARK(6);  // prologue (gray 8 rows, blur 4, Sobel 2)
   for (int Y = ya; Y < yb; Y += SR) {
     const int n = min(SR, yb - Y);
     const bool more = Y + SR < yb;
@@ -655,20 +677,26 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
     // s.g rows 0..7 hold gray [Y-4, Y+4); new gray rows [Y+4, Y+4+n) -> rows 8 ..
     band_gray<CH, F64>(p, s, v, x0, Y + 4, 8, n, pol_in);
     __syncthreads();
+    if (more) PHASE_MARK(0);
+    else PHASE_MARK(5);  // the last sub-step's gray phase carries the next-task claim
     // s.b rows 0..3 hold blurred [Y-2, Y+2); new rows [Y+2, Y+2+n) -> rows 4 ..
     band_blur<FAST, CH>(p, s, x0, Y + 2, 4, n);
     __syncthreads();
+    PHASE_MARK(1);
     // s.q rows 0..1 hold Sobel [Y-1, Y+1); new rows [Y+1, Y+1+n) -> rows 2 ..; meanwhile keep
     // gray rows [Y+n-4, Y+n+4) for the next sub-step
     if (p.nms) band_sobel<true>(p, s, x0, Y + 1, 2, n);
     else band_sobel<false>(p, s, x0, Y + 1, 2, n);
     if (more) shift_rows<double, GWP>(s.g, n, 8);
     __syncthreads();
+    PHASE_MARK(2);
     band_nms_decide(p, s, v, x0, xw, cb, Y, n, parity, pol_mid);
     __syncthreads();
+    PHASE_MARK(3);
     band_nms_finish(p, s, v, x0, Y, parity, pol_mid);
     parity ^= 1;
     __syncthreads();
+    PHASE_MARK(4);
     if (more) {  // context rows for the next sub-step (read by the next blur / NMS)
       shift_rows<double, BWP>(s.b, n, 4);
       shift_rows<unsigned, MWP>(s.q, n, 2, 4);
@@ -1609,6 +1637,26 @@ int igs_debug_edge_trace(void* buf, int64_t capacity, int64_t* written) {
   IGS_CUDA_TRY(cudaMemcpyToSymbol(edge::g_trace_cap, &cap, sizeof(cap)));
   IGS_CUDA_TRY(cudaMemcpyToSymbol(edge::g_trace_n, &zero, sizeof(zero)));
   return IGS_OK;
+}
+
+// Debug (library built with -DIGS_PHASE_PROF): per-phase nanoseconds of the band sub-steps
+// summed over blocks since the last reset: gray, blur, Sobel, NMS decide, NMS finish.
+int igs_debug_edge_phases(uint64_t* out8, int reset) {
+#ifdef IGS_PHASE_PROF
+  unsigned long long h[8];
+  IGS_CUDA_TRY(cudaMemcpyFromSymbol(h, edge::g_phase_ns, sizeof(h)));
+  if (out8)
+    for (int i = 0; i < 8; ++i) out8[i] = h[i];
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    IGS_CUDA_TRY(cudaMemcpyToSymbol(edge::g_phase_ns, z, sizeof(z)));
+  }
+  return IGS_OK;
+#else
+  (void)out8;
+  (void)reset;
+  return IGS_ERR_UNSUPPORTED;
+#endif
 }
 
 int igs_median_normalize(const double* in, int64_t batch, int64_t n, double* out,
