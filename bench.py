@@ -347,6 +347,8 @@ def e2e_edge(args, world, dev):
     return {"value": round(world * VIEWS * PX / sec / 1e6, 3), "unit": "MPix/s",
             "h2d_bytes_per_step": VIEWS * PX * 24, "d2h_bytes_per_step": VIEWS * PX * 8,
             "ms_per_step": round(sec * 1e3, 3), "steps": steps,
+            "h2d_GBps": round(VIEWS * PX * 24 / sec / 1e9, 1),
+            "bound": "PCIe host->device copy of the float64 views (the kernel takes ~4% of the step)",
             "api": "importance_batch(pinned host views, out=pinned host maps), 8-view chunks "
                    "with H2D / kernel / D2H overlapped on three streams"}
 
