@@ -163,7 +163,8 @@ int igs_select_shard_finalize(int64_t n, const int64_t* all_ties, int rank, uint
 int igs_las_workspace_bytes(int64_t count, size_t* bytes);
 
 /* Pre-pass over the mask (1 byte per Gaussian): per-block split counts and their exclusive
- * scan (slot ranks), plus the flags of enum igs_las_flags over the MASKED parents.
+ * scan (slot ranks), plus the flags of enum igs_las_flags over the MASKED parents
+ * (rotations may be NULL: a 2-D scene, no quaternion checks).
  * summary (device int64[2]) receives {n_split, flags}.  Nothing in the scene is written. */
 int igs_las_prepare(const uint8_t* mask, const float* rotations, const float* opacity_logits,
                     int64_t count, float beta, void* workspace, size_t workspace_bytes,
@@ -180,6 +181,14 @@ int igs_las_apply(float* positions, float* log_scales, float* rotations, float* 
                   const uint8_t* mask, float alpha, float log_alpha, float log_gamma,
                   float beta, int renormalize, void* workspace, size_t workspace_bytes,
                   void* stream);
+
+/* 2-D Long-Axis-Split (las_split.py:182-197), after igs_las_prepare with rotations = NULL
+ * (no quaternion checks).  Columns: positions (cap,2), log_scales (cap,2), thetas (cap,),
+ * opacity_logits (cap,), colors (cap,3), float32; the same slot rule as igs_las_apply. */
+int igs_las2d_apply(float* positions, float* log_scales, float* thetas, float* opacity_logits,
+                    float* colors, int64_t count, int64_t capacity, const uint8_t* mask,
+                    float alpha, float log_alpha, float log_gamma, float beta, void* workspace,
+                    size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

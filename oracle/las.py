@@ -125,3 +125,52 @@ def las_split_batch(scene, mask, alpha=0.5, gamma_axis=0.85, beta=0.6):
     out["opacity_logits"] = np.concatenate([out["opacity_logits"], co])
     out["sh"] = np.concatenate([out["sh"], scene["sh"][idx]])
     return out
+
+
+def split_columns_2d(positions, log_scales, thetas, opacity_logits,
+                     alpha=0.5, gamma_axis=0.85, beta=0.6):
+    """_split_common + _split2_columns (las_split.py:78-99, 109-117): the long-axis column of
+    the 2-D rotation [[cos, -sin], [sin, cos]] -- (cos, sin) for axis 0, (-sin, cos) for 1."""
+    dt = log_scales.dtype.type
+    log_alpha, log_gamma = dt(math.log(alpha)), dt(math.log(gamma_axis))
+    rows = np.arange(len(log_scales))
+    l_idx = np.argmax(log_scales, axis=-1)
+    long_ls = log_scales[rows, l_idx]
+    offset = np.exp(long_ls) * dt(alpha)
+    child_ls = log_scales + log_gamma
+    child_ls[rows, l_idx] = long_ls + log_alpha
+    child_o = logit(sigmoid(opacity_logits) * dt(beta)).astype(log_scales.dtype, copy=False)
+    c, s = np.cos(thetas), np.sin(thetas)
+    column = np.where((l_idx == 0)[:, None], np.stack([c, s], -1), np.stack([-s, c], -1))
+    disp = column * offset[:, None]
+    return positions + disp, positions - disp, child_ls, child_o
+
+
+def las_split_batch_2d(scene, mask, alpha=0.5, gamma_axis=0.85, beta=0.6):
+    """las_split.py:182-197 on a dict scene (positions (N,2), log_scales (N,2), thetas (N,),
+    opacity_logits (N,), colors (N,3), capacity); returns a NEW dict."""
+    check_constants(alpha, gamma_axis, beta)
+    n = len(scene["positions"])
+    mask = np.asarray(mask, dtype=bool)
+    if mask.shape != (n,):
+        raise ValueError(f"mask length {mask.shape} does not match scene count {n}")
+    k = int(mask.sum())
+    if n + k > scene["capacity"]:
+        raise BudgetError(f"splitting {k} of {n} primitives exceeds capacity {scene['capacity']}")
+    out = {key: (np.array(v, copy=True) if isinstance(v, np.ndarray) else v)
+           for key, v in scene.items()}
+    if k == 0:
+        return out
+    idx = np.flatnonzero(mask)
+    pa, pb, cls, co = split_columns_2d(scene["positions"][idx], scene["log_scales"][idx],
+                                       scene["thetas"][idx], scene["opacity_logits"][idx],
+                                       alpha, gamma_axis, beta)
+    out["positions"][idx] = pa
+    out["log_scales"][idx] = cls
+    out["opacity_logits"][idx] = co
+    out["positions"] = np.concatenate([out["positions"], pb])
+    out["log_scales"] = np.concatenate([out["log_scales"], cls])
+    out["thetas"] = np.concatenate([out["thetas"], scene["thetas"][idx]])
+    out["opacity_logits"] = np.concatenate([out["opacity_logits"], co])
+    out["colors"] = np.concatenate([out["colors"], scene["colors"][idx]])
+    return out

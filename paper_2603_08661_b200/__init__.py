@@ -8,14 +8,15 @@ hand-written CUDA kernels in ``libigs_b200.so`` (C ABI: ``include/igs_b200.h``),
 bound with ctypes.  There is no CPU fallback.
 """
 
-from .core import Scene3
+from .core import Scene2, Scene3
 from .densify_controller import (EVENT_CSV_HEADER, DensifyEvent, DensifyStats,
                                  accumulate_grads, accumulate_position_grads, densify_step,
                                  select_candidates)
 from .edge_pipeline import (GradientField, blur_kernel_5x5, gaussian_blur_5x5,
                             importance_batch, importance_pipeline, median_normalize,
                             nms_thin, sample_scores, sobel_gradients, to_grayscale)
-from .las_split import BudgetError, SplitConstants, las_split_batch, principal_axis
+from .las_split import (BudgetError, SplitConstants, las_split_batch, las_split_batch_2d,
+                        principal_axis)
 from .schedule import DensifyConfig, is_densify_step, is_warmup_step
 
 __version__ = "0.1.0"

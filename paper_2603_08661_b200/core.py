@@ -150,3 +150,70 @@ class Scene3:
         if n > self.capacity:
             raise ValueError(f"count {n} exceeds capacity {self.capacity}")
         self._count = int(n)
+
+
+class Scene2:
+    """GPU 2-D scene (``splitkit.core.Scene2``, core.py:203-244): float32 SoA columns
+    ``positions`` (N,2), ``log_scales`` (N,2), ``thetas`` (N,), ``opacity_logits`` (N,),
+    ``colors`` (N,3), pre-reserved at ``capacity`` rows."""
+
+    _columns = ("positions", "log_scales", "thetas", "opacity_logits", "colors")
+
+    def __init__(self, positions, log_scales, thetas, opacity_logits, colors, capacity,
+                 dtype=np.float32, device=None):
+        if capacity < 1:
+            raise ValueError("capacity must be positive")
+        if np.dtype(dtype) != np.float32:
+            raise ValueError("the B200 scene stores float32 columns")
+        dev = _dev(device)
+        f = torch.float32
+        cols = {"positions": _col(positions, 2, f, dev), "log_scales": _col(log_scales, 2, f, dev),
+                "thetas": _col(thetas, 0, f, dev), "opacity_logits": _col(opacity_logits, 0, f, dev),
+                "colors": _col(colors, 3, f, dev)}
+        n = cols["positions"].shape[0]
+        for name, col in cols.items():
+            if col.shape[0] != n:
+                raise ValueError(f"column {name} has length {col.shape[0]} != {n}")
+        self.capacity = int(capacity)
+        if n > self.capacity:
+            raise ValueError(f"count {n} exceeds capacity {self.capacity}")
+        self._cols = {}
+        for name, col in cols.items():
+            buf = torch.empty((self.capacity,) + tuple(col.shape[1:]), dtype=f, device=dev)
+            buf[:n] = col
+            self._cols[name] = buf
+        self._count = n
+
+    @property
+    def count(self) -> int:
+        return self._count
+
+    @property
+    def device(self):
+        return self._cols["positions"].device
+
+    def __getattr__(self, name):
+        cols = self.__dict__.get("_cols")
+        if cols is not None and name in cols:
+            return cols[name][: self._count]
+        raise AttributeError(name)
+
+    def validate(self):
+        if self._count > self.capacity:
+            raise ValueError(f"count {self._count} exceeds capacity {self.capacity}")
+        return self
+
+    def to_numpy(self) -> dict:
+        out = {k: getattr(self, k).cpu().numpy() for k in self._columns}
+        out["capacity"] = self.capacity
+        return out
+
+    @classmethod
+    def from_reference(cls, scene, device=None) -> "Scene2":
+        return cls(scene.positions, scene.log_scales, scene.thetas, scene.opacity_logits,
+                   scene.colors, scene.capacity, device=device)
+
+    def _set_count(self, n: int):
+        if n > self.capacity:
+            raise ValueError(f"count {n} exceeds capacity {self.capacity}")
+        self._count = int(n)

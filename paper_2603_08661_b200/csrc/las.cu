@@ -73,10 +73,12 @@ __global__ void __launch_bounds__(NT) las_prepare_kernel(const uint8_t* __restri
     long long i = base + j * NT + threadIdx.x;
     if (i < count && mask[i]) {
       ++local;
-      float4 q = reinterpret_cast<const float4*>(rot)[i];
-      float n = quat_norm(q);
-      if (!isfinite(n) || n == 0.0f) flags |= IGS_LAS_BAD_QUAT;
-      else if (fabsf(n - 1.0f) > 1e-4f) flags |= IGS_LAS_RENORM;
+      if (rot) {  // 3-D scenes: quaternion checks (2-D scenes pass rot = nullptr)
+        float4 q = reinterpret_cast<const float4*>(rot)[i];
+        float n = quat_norm(q);
+        if (!isfinite(n) || n == 0.0f) flags |= IGS_LAS_BAD_QUAT;
+        else if (fabsf(n - 1.0f) > 1e-4f) flags |= IGS_LAS_RENORM;
+      }
       float r = raw_opacity(opac[i], beta);
       if (!(r > 0.0f && r < 1.0f)) flags |= IGS_LAS_BAD_OPACITY;
     }
@@ -271,6 +273,79 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
   }
 }
 
+// 2-D Long-Axis-Split (las_split.py:109-117, 182-197): the same slot rule and scale/opacity
+// update; the displacement is column l of [[cos, -sin], [sin, cos]] (theta float32).
+__global__ void __launch_bounds__(NT) las2d_apply_kernel(
+    float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ theta,
+    float* __restrict__ opac, float* __restrict__ col, long long count,
+    const uint8_t* __restrict__ mask, Consts c, const unsigned long long* __restrict__ tile_off) {
+  __shared__ unsigned warp_cnt[PER * NT / 32];
+  __shared__ unsigned warp_pre[PER * NT / 32];
+  const long long base = (long long)blockIdx.x * TILE;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  bool m[PER];
+  unsigned wrank[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    long long i = base + j * NT + threadIdx.x;
+    m[j] = i < count && mask[i];
+    unsigned bal = __ballot_sync(0xffffffffu, m[j]);
+    wrank[j] = __popc(bal & lanemask_lt());
+    if (lane == 0) warp_cnt[j * (NT / 32) + warp] = __popc(bal);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned v = warp_cnt[threadIdx.x];
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (threadIdx.x >= (unsigned)o) x += y;
+    }
+    warp_pre[threadIdx.x] = x - v;
+  }
+  __syncthreads();
+  const unsigned long long slot0 = (unsigned long long)count + tile_off[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    if (!m[j]) continue;
+    const long long i = base + j * NT + threadIdx.x;
+    const long long dst = (long long)(slot0 + warp_pre[j * (NT / 32) + warp] + wrank[j]);
+    const float l0 = ls[2 * i], l1 = ls[2 * i + 1];
+    int l = 0;  // np.argmax: first maximum (a NaN counts as the maximum)
+    float best = l0;
+    if (!(best != best) && (l1 > best || l1 != l1)) {
+      l = 1;
+      best = l1;
+    }
+    const float offset = expf(best) * c.alpha;
+    float cl0 = l0 + c.log_gamma, cl1 = l1 + c.log_gamma;
+    const float cll = best + c.log_alpha;
+    if (l == 0) cl0 = cll;
+    else cl1 = cll;
+    const float raw = raw_opacity(opac[i], c.beta);
+    const float co = logf(raw / (1.0f - raw));
+    const float th = theta[i];
+    const float ct = cosf(th), st = sinf(th);
+    const float d0 = (l == 0 ? ct : -st) * offset, d1 = (l == 0 ? st : ct) * offset;
+    const float p0 = pos[2 * i], p1 = pos[2 * i + 1];
+    pos[2 * i] = p0 + d0;
+    pos[2 * i + 1] = p1 + d1;
+    ls[2 * i] = cl0;
+    ls[2 * i + 1] = cl1;
+    opac[i] = co;
+    pos[2 * dst] = p0 - d0;
+    pos[2 * dst + 1] = p1 - d1;
+    ls[2 * dst] = cl0;
+    ls[2 * dst + 1] = cl1;
+    theta[dst] = th;
+    opac[dst] = co;
+    col[3 * dst] = col[3 * i];
+    col[3 * dst + 1] = col[3 * i + 1];
+    col[3 * dst + 2] = col[3 * i + 2];
+  }
+}
+
 }  // namespace las
 }  // namespace igs
 
@@ -288,8 +363,8 @@ int igs_las_prepare(const uint8_t* mask, const float* rotations, const float* op
                     int64_t count, float beta, void* workspace, size_t workspace_bytes,
                     int64_t* summary, void* stream) {
   if (count < 0 || !summary) return IGS_ERR_ARGUMENT;
-  if (count > 0 && (!mask || !rotations || !opacity_logits)) return IGS_ERR_ARGUMENT;
-  if (count > 0 && ((uintptr_t)rotations & 15)) return IGS_ERR_ARGUMENT;
+  if (count > 0 && (!mask || !opacity_logits)) return IGS_ERR_ARGUMENT;
+  if (count > 0 && ((uintptr_t)rotations & 15)) return IGS_ERR_ARGUMENT;  // nullable: 2-D
   las::Layout L = las::layout(count);
   if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
@@ -324,6 +399,25 @@ int igs_las_apply(float* positions, float* log_scales, float* rotations, float* 
   las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
       positions, log_scales, rotations, opacity_logits, sh, sh_floats, count, mask, c,
       renormalize, (const unsigned long long*)((char*)workspace + L.tile_off));
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
+int igs_las2d_apply(float* positions, float* log_scales, float* thetas, float* opacity_logits,
+                    float* colors, int64_t count, int64_t capacity, const uint8_t* mask,
+                    float alpha, float log_alpha, float log_gamma, float beta, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  if (count < 0 || capacity < count) return IGS_ERR_ARGUMENT;
+  if (count == 0) return IGS_OK;
+  if (!positions || !log_scales || !thetas || !opacity_logits || !colors || !mask)
+    return IGS_ERR_ARGUMENT;
+  las::Layout L = las::layout(count);
+  if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
+  long long tiles = (count + las::TILE - 1) / las::TILE;
+  las::Consts c{alpha, log_alpha, log_gamma, beta};
+  las::las2d_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
+      positions, log_scales, thetas, opacity_logits, colors, count, mask, c,
+      (const unsigned long long*)((char*)workspace + L.tile_off));
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }

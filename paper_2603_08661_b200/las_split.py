@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .core import Scene3
+from .core import Scene2, Scene3
 
 
 class BudgetError(RuntimeError):
@@ -122,3 +122,35 @@ def principal_axis(log_scale):
     t = log_scale if isinstance(log_scale, torch.Tensor) else torch.as_tensor(np.asarray(log_scale))
     idx = torch.argmax(t, dim=-1)
     return int(idx) if idx.ndim == 0 else idx
+
+
+def las_split_batch_2d(scene: Scene2, mask, c: SplitConstants = SplitConstants()) -> Scene2:
+    """2-D analogue of :func:`las_split_batch` on a GPU scene (las_split.py:182-197): masked
+    parents take the +offset child in place, -offset children are appended in parent order."""
+    if not isinstance(scene, Scene2):
+        raise TypeError(f"expected a paper_2603_08661_b200.core.Scene2, got {type(scene).__name__}")
+    L = _lib.lib()
+    m = _mask_tensor(mask, scene.count, scene.device)
+    nbytes = _lib.query_size(L.igs_las_workspace_bytes, scene.count)
+    ws = _lib.workspace(nbytes, scene.device, "las")
+    summary = torch.empty(2, dtype=torch.int64, device=scene.device)
+    alpha, log_alpha, log_gamma, beta = c.device_constants()
+    cols = scene._cols
+    _lib.check(L.igs_las_prepare(m.data_ptr(), None, cols["opacity_logits"].data_ptr(),
+                                 scene.count, beta, ws.data_ptr(), ws.numel(),
+                                 summary.data_ptr(), _lib.stream_handle()), "las_split_batch_2d")
+    n_split, flags = (int(v) for v in summary.cpu().tolist())
+    if scene.count + n_split > scene.capacity:
+        raise BudgetError(f"splitting {n_split} of {scene.count} primitives exceeds "
+                          f"capacity {scene.capacity}")
+    if n_split == 0:
+        return scene
+    if flags & _lib.IGS_LAS_BAD_OPACITY:
+        raise ValueError("logit requires all values strictly inside (0, 1)")
+    _lib.check(L.igs_las2d_apply(cols["positions"].data_ptr(), cols["log_scales"].data_ptr(),
+                                 cols["thetas"].data_ptr(), cols["opacity_logits"].data_ptr(),
+                                 cols["colors"].data_ptr(), scene.count, scene.capacity,
+                                 m.data_ptr(), alpha, log_alpha, log_gamma, beta, ws.data_ptr(),
+                                 ws.numel(), _lib.stream_handle()), "las_split_batch_2d")
+    scene._set_count(scene.count + n_split)
+    return scene.validate()

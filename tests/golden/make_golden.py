@@ -19,14 +19,15 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from splitkit.core import Scene3  # noqa: E402
+from splitkit.core import Scene2, Scene3  # noqa: E402
 from splitkit.densify_controller import (DensifyStats, accumulate_grads,  # noqa: E402
                                          densify_step, select_candidates)
 from splitkit.edge_pipeline import (GradientField, gaussian_blur_5x5,  # noqa: E402
                                     importance_pipeline, median_normalize,
                                     nms_thin, sample_scores, sobel_gradients,
                                     to_grayscale)
-from splitkit.las_split import BudgetError, SplitConstants, las_split_batch  # noqa: E402
+from splitkit.las_split import (BudgetError, SplitConstants, las_split_batch,  # noqa: E402
+                                las_split_batch_2d)
 from splitkit.schedule import DensifyConfig  # noqa: E402
 
 
@@ -251,6 +252,31 @@ def select_cases():
     return out
 
 
+def las2d_cases():
+    """las_split_batch_2d (las_split.py:182-197) on random 2-D scenes."""
+    out = {}
+    rng = np.random.default_rng(606)
+    specs = [("c%d" % i, int(rng.integers(1, 80)), 0.5) for i in range(20)]
+    specs += [("all1k", 1000, 1.0), ("sparse1k", 1000, 0.05), ("empty", 30, 0.0)]
+    for name, n, p in specs:
+        ls = rng.uniform(-0.7, 0.7, (n, 2))
+        if name == "c0":
+            ls[:, 1] = ls[:, 0]  # argmax ties -> axis 0
+        scene = Scene2(rng.normal(0, 1, (n, 2)), ls, rng.uniform(-np.pi, np.pi, n),
+                       rng.normal(0, 1.5, n), rng.random((n, 3)), capacity=2 * n + 1)
+        mask = rng.random(n) < p
+        before = scene.copy()
+        consts = SplitConstants(alpha=0.3, gamma_axis=0.9, beta=0.7) if name == "c1" else SplitConstants()
+        las_split_batch_2d(scene, mask, consts)
+        for col in ("positions", "log_scales", "thetas", "opacity_logits", "colors"):
+            out[f"{name}/in_{col}"] = getattr(before, col)
+            out[f"{name}/out_{col}"] = getattr(scene, col)
+        out[f"{name}/mask"] = mask
+        out[f"{name}/capacity"] = np.int64(before.capacity)
+        out[f"{name}/constants"] = np.array([consts.alpha, consts.gamma_axis, consts.beta])
+    return out
+
+
 def sample_cases():
     """sample_scores (edge_pipeline.py:138-164): bilinear sampling, outside -> 0."""
     out = {}
@@ -279,7 +305,8 @@ def sample_cases():
 
 def main():
     for name, fn in (("edge", edge_cases), ("nms", nms_cases), ("median", median_cases),
-                     ("las", las_cases), ("select", select_cases), ("sample", sample_cases)):
+                     ("las", las_cases), ("select", select_cases), ("sample", sample_cases),
+                     ("las2d", las2d_cases)):
         data = fn()
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **data)
         print(name, len(data), "arrays")

@@ -158,3 +158,41 @@ def test_batch_equals_sequential_random_scenes():
         s = gpu_scene(d)
         b.las_split_batch(s, mask)
         assert_las_close(s.to_numpy(), OL.las_split_batch(d, mask))
+
+
+LAS2D = load_golden("las2d")
+
+
+@pytest.mark.parametrize("case", sorted(LAS2D))
+def test_golden_las2d(case):
+    """las_split_batch_2d: log-scales, thetas, colours bit-exact; positions / opacities within
+    the north-star tolerance (numpy's float32 exp / log / sin / cos are not correctly rounded)."""
+    b = B()
+    c = LAS2D[case]
+    sc = b.Scene2(c["in_positions"], c["in_log_scales"], c["in_thetas"], c["in_opacity_logits"],
+                  c["in_colors"], capacity=int(c["capacity"]))
+    a, g, be = (float(x) for x in c["constants"])
+    b.las_split_batch_2d(sc, c["mask"], b.SplitConstants(alpha=a, gamma_axis=g, beta=be))
+    got = sc.to_numpy()
+    for k in ("log_scales", "thetas", "colors"):
+        assert_array_equal(got[k], c[f"out_{k}"], err_msg=k)
+    want_p, p_in = c["out_positions"], c["in_positions"]
+    n = len(p_in)
+    scale = np.abs(want_p).copy()
+    scale[:n] += np.abs(want_p[:n] - p_in)
+    assert (np.abs(got["positions"] - want_p) <= 1e-5 * (scale + 1e-30) + 1e-7).all()
+    wo = c["out_opacity_logits"]
+    assert (np.abs(got["opacity_logits"] - wo) <= 1e-5 * np.maximum(1.0, np.abs(wo))).all()
+
+
+def test_las2d_errors():
+    b = B()
+    sc = b.Scene2(np.zeros((4, 2)), np.zeros((4, 2)), np.zeros(4), np.zeros(4), np.zeros((4, 3)),
+                  capacity=5)
+    with pytest.raises(b.BudgetError):
+        b.las_split_batch_2d(sc, np.ones(4, bool))
+    with pytest.raises(ValueError):
+        b.las_split_batch_2d(sc, np.ones(3, bool))
+    assert sc.count == 4
+    b.las_split_batch_2d(sc, np.zeros(4, bool))
+    assert sc.count == 4

@@ -167,3 +167,14 @@ def test_sample_scores_known_answers():
                        [0.0, 11.0])
     with pytest.raises(IndexError):
         OE.sample_scores(imp, [[np.nan, 1.0]])
+
+
+def test_las2d_bit_exact_vs_reference():
+    for name, c in load_golden("las2d").items():
+        scene = {k: c[f"in_{k}"] for k in ("positions", "log_scales", "thetas", "opacity_logits",
+                                           "colors")}
+        scene["capacity"] = int(c["capacity"])
+        a, g, b = (float(x) for x in c["constants"])
+        out = OL.las_split_batch_2d(scene, c["mask"], a, g, b)
+        for k in ("positions", "log_scales", "thetas", "opacity_logits", "colors"):
+            assert_array_equal(out[k], c[f"out_{k}"], err_msg=f"{name} {k}")
