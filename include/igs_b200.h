@@ -190,6 +190,14 @@ int igs_las2d_apply(float* positions, float* log_scales, float* thetas, float* o
                     float alpha, float log_alpha, float log_gamma, float beta, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* ---- scene files (io_cli.py:83-134) ------------------------------------- */
+
+/* read_scene's quaternion renormalisation (io_cli.py:122-127), in place on n float32
+ * quaternions (16-byte aligned): q = float32(float64(q) / ||float64(q)||), the norm summed
+ * left to right (np.linalg.norm).  flags (device int32) receives bit 1 for a zero or
+ * non-finite norm (SceneFormatError). */
+int igs_normalize_quaternions(float* quats, int64_t n, int32_t* flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

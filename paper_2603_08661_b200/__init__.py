@@ -17,6 +17,8 @@ from .edge_pipeline import (GradientField, blur_kernel_5x5, gaussian_blur_5x5,
                             nms_thin, sample_scores, sobel_gradients, to_grayscale)
 from .las_split import (BudgetError, SplitConstants, las_split_batch, las_split_batch_2d,
                         principal_axis)
+from .scene_io import (BadMagicError, FormatError, SceneFormatError, SizeMismatchError,
+                       UnsupportedVersionError, read_scene, scene_bytes, write_scene)
 from .schedule import DensifyConfig, is_densify_step, is_warmup_step
 
 __version__ = "0.1.0"

@@ -39,6 +39,7 @@ SIGNATURES = {
     "igs_sobel_gradients": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "igs_nms_thin": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "igs_median_normalize": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "igs_normalize_quaternions": (_int, [_vp, _i64, _vp, _vp]),
     "igs_sample_scores": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp]),
     "igs_debug_edge_trace": (_int, [_vp, _i64, C.POINTER(C.c_int64)]),
     "igs_debug_edge_phases": (_int, [_vp, _int]),

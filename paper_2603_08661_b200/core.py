@@ -55,7 +55,7 @@ class Scene3:
         op = _col(opacity_logits, 0, f, dev)
         c = torch.as_tensor(np.asarray(colors) if not isinstance(colors, torch.Tensor) else colors)
         c = c.to(device=dev, dtype=f)
-        sh = c.reshape(c.shape[0], -1, 3) if c.ndim == 3 else c.reshape(-1, 1, 3)
+        sh = c if c.ndim == 3 else c.reshape(-1, 1, 3)
         n = pos.shape[0]
         self.capacity = int(capacity)
         for name, col in (("log_scales", ls), ("rotations", rot), ("opacity_logits", op),

@@ -22,6 +22,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from splitkit.core import Scene2, Scene3  # noqa: E402
 from splitkit.densify_controller import (DensifyStats, accumulate_grads,  # noqa: E402
                                          densify_step, select_candidates)
+from splitkit.io_cli import read_scene, scene_bytes  # noqa: E402
 from splitkit.edge_pipeline import (GradientField, gaussian_blur_5x5,  # noqa: E402
                                     importance_pipeline, median_normalize,
                                     nms_thin, sample_scores, sobel_gradients,
@@ -303,10 +304,74 @@ def sample_cases():
     return out
 
 
+def igsp_cases():
+    """.igsp scene files (io_cli.py:83-134): the reference's bytes for random scenes, what its
+    reader returns for them (quaternions renormalised), and the exception each corrupt file
+    raises."""
+    import tempfile
+    out = {}
+    rng = np.random.default_rng(707)
+    s3 = random_scene(rng, 257, 300)
+    q = s3.rotations.copy()
+    q[:40] *= rng.uniform(0.2, 5.0, (40, 1)).astype(np.float32)
+    q[40:45] *= np.float32(1e-20)
+    q[45:50] *= np.float32(1e18)
+    s3.rotations[...] = q
+    s2 = Scene2(rng.normal(0, 1, (99, 2)), rng.uniform(-0.7, 0.7, (99, 2)),
+                rng.uniform(-np.pi, np.pi, 99), rng.normal(0, 1.5, 99), rng.random((99, 3)),
+                capacity=99)
+    empty = Scene3(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 4)), np.zeros(0),
+                   np.zeros((0, 3)), capacity=1)
+    files = {}
+    with tempfile.TemporaryDirectory() as d:
+        for name, scene in (("scene3", s3), ("scene2", s2), ("empty3", empty)):
+            data = scene_bytes(scene)
+            files[name] = data
+            path = os.path.join(d, name + ".igsp")
+            with open(path, "wb") as fh:
+                fh.write(data)
+            back = read_scene(path)
+            cols = ("positions", "log_scales", "rotations" if name != "scene2" else "thetas",
+                    "opacity_logits", "colors")
+            for col in cols:
+                out[f"{name}/in_{col}"] = getattr(scene, col)
+                out[f"{name}/read_{col}"] = getattr(back, col)
+            out[f"{name}/capacity"] = np.int64(back.capacity)
+        good = files["scene3"]
+        zero = bytearray(good)
+        qoff = 15 + 6 * 257 * 4
+        zero[qoff + 16 * 7: qoff + 16 * 8] = bytes(16)
+        nan = bytearray(good)
+        nan[qoff: qoff + 4] = np.array([np.nan], "<f4").tobytes()
+        bad = {
+            "bad_magic": b"IGSQ" + good[4:], "short_magic": b"IG", "empty_file": b"",
+            "short_header": good[:10], "version": good[:4] + b"\x07\x00" + good[6:],
+            "dims": good[:6] + b"\x04" + good[7:], "extra_byte": good + b"\x00",
+            "missing_byte": good[:-1], "zero_quat": bytes(zero), "nan_quat": bytes(nan),
+            "count_big": good[:7] + np.array([258], "<u8").tobytes() + good[15:],
+        }
+        names = []
+        for name, data in bad.items():
+            path = os.path.join(d, name + ".igsp")
+            with open(path, "wb") as fh:
+                fh.write(data)
+            try:
+                read_scene(path)
+                err = "none"
+            except Exception as e:  # noqa: BLE001
+                err = type(e).__name__
+            names.append(name)
+            out[f"bad/{name}/bytes"] = np.frombuffer(data, np.uint8)
+            out[f"bad/{name}/error"] = np.array(err)
+    for name, data in files.items():
+        out[f"{name}/bytes"] = np.frombuffer(data, np.uint8)
+    return out
+
+
 def main():
     for name, fn in (("edge", edge_cases), ("nms", nms_cases), ("median", median_cases),
                      ("las", las_cases), ("select", select_cases), ("sample", sample_cases),
-                     ("las2d", las2d_cases)):
+                     ("las2d", las2d_cases), ("igsp", igsp_cases)):
         data = fn()
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **data)
         print(name, len(data), "arrays")

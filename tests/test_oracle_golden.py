@@ -178,3 +178,27 @@ def test_las2d_bit_exact_vs_reference():
         out = OL.las_split_batch_2d(scene, c["mask"], a, g, b)
         for k in ("positions", "log_scales", "thetas", "opacity_logits", "colors"):
             assert_array_equal(out[k], c[f"out_{k}"], err_msg=f"{name} {k}")
+
+
+def test_igsp_layout_vs_reference():
+    """Scene-file bytes and the reader's renormalised columns (io_cli.py:83-134)."""
+    from oracle import scene_io as OI
+    g = load_golden("igsp")
+    for name in ("scene3", "scene2", "empty3"):
+        c = g[name]
+        dims = 2 if name == "scene2" else 3
+        rot = "thetas" if dims == 2 else "rotations"
+        cols = {k: c[f"in_{k}"] for k in ("positions", "log_scales", rot, "opacity_logits",
+                                          "colors")}
+        data = c["bytes"].tobytes()
+        assert OI.scene_bytes(dims, cols) == data, name
+        d, back = OI.read_scene_bytes(data)
+        assert d == dims
+        for k, v in back.items():
+            assert_array_equal(v, c[f"read_{k}"], err_msg=f"{name} {k}")
+    bad = g["bad"]
+    for key in sorted(k for k in bad if k.endswith("/error")):
+        case = key.split("/")[0]
+        with pytest.raises(OI.OracleFormatError) as e:
+            OI.read_scene_bytes(bad[f"{case}/bytes"].tobytes())
+        assert e.value.kind == str(bad[key]), case
