@@ -477,9 +477,15 @@ __device__ void band_sobel(const Params& p, Smem& s, int x0, int y_first, int rq
       m[k] = d[k];
     }
   };
+  if (nr == SH && y0 >= 0 && y0 + SH <= H) {
+    // common case: straight-line code, so the window shift is register renaming
 #pragma unroll
-  for (int j = 0; j < SH; ++j)
-    if (j < nr) row(j, true);
+    for (int j = 0; j < SH; ++j) row(j, false);
+  } else {
+#pragma unroll
+    for (int j = 0; j < SH; ++j)
+      if (j < nr) row(j, true);
+  }
 }
 
 // Exact glibc hypot at magnitude cell (s.q row rq, column c) of image row y (0 outside).
