@@ -184,6 +184,12 @@ __device__ __forceinline__ double ld_hint(const float* a, unsigned long long pol
 __device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
+// predicated form: no divergent branch (BSSY/BSYNC) around the store
+__device__ __forceinline__ void st_hint_if(bool pred, double* a, double v, unsigned long long pol) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+               "@p st.global.L2::cache_hint.f64 [%0], %1, %2;\n\t}" ::"l"(a), "d"(v), "l"(pol),
+               "r"((int)pred) : "memory");
+}
 __device__ __forceinline__ double ld_cg_hint(const double* a, unsigned long long pol) {
   double v;
   asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
@@ -545,7 +551,7 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
         need = need && in;
         // every pixel gets a full-line store here (0); survivors are overwritten by finish
         // (no median) or by the apply pass (median), so no line is ever partially written
-        if ((p.median || !need) && in) st_hint(orow + c, 0.0, pol_mid);
+        st_hint_if((p.median || !need) && in, orow + c, 0.0, pol_mid);
       }
       bal[hh][k] = __ballot_sync(0xffffffffu, need);
       tot[hh] += __popc(bal[hh][k]);
@@ -1180,7 +1186,7 @@ __device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, u
       const unsigned* ib = ibuf + (k % NBUF) * APIECE;
       for (int i = threadIdx.x; i < len; i += NT) {
         const double x = vb[i];
-        if (x != 0.0) st_hint(dst + ib[i], normalise(x, denom, rd, plain), pol_out);
+        st_hint_if(x != 0.0, dst + ib[i], normalise(x, denom, rd, plain), pol_out);
       }
       __syncthreads();
       if (threadIdx.x == 0 && k + NBUF < npieces) {
