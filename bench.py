@@ -311,6 +311,8 @@ def run_ours(args, world, rank, local):
     if not args.no_las:
         line["las"] = bench_las(args, world, dev, peak, peak_src)
         line["densify_sharded"] = bench_densify_sharded(args, world, rank, dev)
+        if rank == 0:
+            line["scene_io"] = bench_scene_io(args, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, procs, _ = cpu_edge_rate(2, 1)
         line["cpu_baseline"] = {"value": round(rate, 3), "unit": "MPix/s", "cores": procs,
@@ -434,6 +436,63 @@ def bench_las(args, world, dev, peak, peak_src):
 
 DENSIFY_N = 6_000_000
 UHD_VIEWS = 128
+
+
+def bench_scene_io(args, dev, n=6_000_000):
+    """.igsp load / save of a 6M-Gaussian colour-only cloud (BASELINE.json configs[3] size,
+    14 floats per record = 336 MB) between a page-cached file and device columns: pinned
+    read + per-column H2D + GPU quaternion renormalisation, and D2H + atomic rename. Host
+    wall clock around synchronised calls (the path is host IO)."""
+    import shutil
+    import tempfile
+
+    import numpy as np
+    import torch
+
+    import paper_2603_08661_b200 as igs
+    rng = np.random.default_rng(11)
+    q = rng.normal(size=(n, 4)).astype(np.float32)
+    sc = igs.Scene3(rng.normal(size=(n, 3)).astype(np.float32),
+                    rng.uniform(-1, 1, (n, 3)).astype(np.float32), q,
+                    rng.normal(size=n).astype(np.float32), rng.random((n, 3)).astype(np.float32),
+                    capacity=n, device=dev)
+    d = tempfile.mkdtemp(prefix="igsp_bench_")
+    try:
+        path = os.path.join(d, "cloud.igsp")
+        igs.write_scene(sc, path)
+        nbytes = os.path.getsize(path)
+        reps = 3
+        for _ in range(1):
+            igs.read_scene(path, capacity=n + n // 20, device=dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            back = igs.read_scene(path, capacity=n + n // 20, device=dev)
+        torch.cuda.synchronize()
+        rd = (time.perf_counter() - t0) / reps
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            igs.write_scene(back, path)
+        wr = (time.perf_counter() - t0) / reps
+        res = {"metric": "scene file GB/s", "gaussians": n, "bytes": nbytes,
+               "read_GBps": round(nbytes / rd / 1e9, 2), "read_ms": round(rd * 1e3, 2),
+               "write_GBps": round(nbytes / wr / 1e9, 2), "write_ms": round(wr * 1e3, 2),
+               "config": {"workload": "read_scene / write_scene, 6M Gaussians, colour-only "
+                                      "records (io_cli.py:83-134), page-cached file in /tmp",
+                          "timing": "host wall clock, 3 reps after 1 warm-up"}}
+        if ref_kind() == "reference" and not args.no_cpu:
+            if REF_PATH not in sys.path:
+                sys.path.insert(0, REF_PATH)
+            from splitkit.io_cli import read_scene as ref_read
+            ref_read(path)
+            t0 = time.perf_counter()
+            ref_read(path)
+            res["cpu_baseline"] = {"read_GBps": round(nbytes / (time.perf_counter() - t0) / 1e9, 2),
+                                   "cores": 1, "kind": "reference",
+                                   "sample": "one splitkit.io_cli.read_scene of the same file"}
+        return res
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
 
 
 def bench_uhd(args, world, dev, peak):

@@ -8,12 +8,12 @@ Layout (little endian): a 15-byte header ``<4sHBQ`` (magic ``IGSP``, version, di
 count), then one float32 block per column in the order positions, log_scales, rotations
 (quaternions in 3-D, angles in 2-D), opacity_logits, colors.
 
-B200 path: the file is read straight into pinned host memory, at an offset that puts
-the payload on a 16-byte boundary, and each column block goes to its pre-reserved
-device column with one asynchronous H2D copy. The rotation block is renormalised in
-place on the GPU (``igs_normalize_quaternions``, bit-identical to the reference's
-float64 numpy arithmetic). Saving reverses this: D2H copies into one pinned buffer,
-then a temp-file rename.
+B200 path: file bytes move in 8 MB pieces through a reusable pool of pinned staging
+slots. Worker threads pread / pwrite at the pieces' final offsets (in parallel: the
+syscalls release the GIL) and issue each piece's H2D / D2H copy on their own CUDA stream,
+straight into / out of the pre-reserved device columns. The rotation block is then
+renormalised in place on the GPU (``igs_normalize_quaternions``, bit-identical to the
+reference's float64 numpy arithmetic). Writes go to a temp file that is renamed into place.
 
 Extension (version 2): a ``Scene3`` with ``K > 1`` spherical-harmonic triplets per
 Gaussian cannot be stored in the reference's 14-float record (:36). It is written as
@@ -76,51 +76,129 @@ def _columns(scene):
     raise TypeError(f"expected Scene2 or Scene3, got {type(scene).__name__}")
 
 
-def _pinned(nbytes: int, header_len: int):
-    """Pinned uint8 buffer whose byte `pad + header_len` is 16-byte aligned; returns (buf, pad)."""
-    pad = (-header_len) % 16
-    buf = torch.empty(pad + nbytes, dtype=torch.uint8, pin_memory=True)
-    return buf, pad
+# ---- chunked pinned pipeline ---------------------------------------------------------
+# File bytes move in CHUNK-sized pieces through a reusable pool of pinned staging slots:
+# worker threads pread / pwrite (the syscalls release the GIL, so page-cache copies run in
+# parallel) and issue the H2D / D2H copy of their slot on their own CUDA stream.
+CHUNK = 8 << 20
+_WORKERS = max(1, min(8, os.cpu_count() or 1))
+_POOL = {}
 
 
-def _pack(scene):
-    """Serialise into a pinned buffer; returns (buf, start, end)."""
+def _slots(device):
+    key = (device.index, _WORKERS)
+    if key not in _POOL:
+        _POOL[key] = [[torch.empty(CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+                      for _ in range(_WORKERS)]
+    return _POOL[key]
+
+
+def _segments(cols, base):
+    """[(file offset, device byte view)] for contiguous device columns laid out from `base`."""
+    segs, off = [], base
+    for t in cols:
+        b = t.reshape(-1).view(torch.uint8)
+        for a in range(0, b.numel(), CHUNK):
+            segs.append((off + a, b[a:a + CHUNK]))
+        off += b.numel()
+    return segs, off
+
+
+def _run_chunks(segs, device, fn):
+    """Run fn(slot, file_off, dev_bytes, stream) over the segments on the worker pool; the
+    caller's stream waits for every worker stream."""
+    if not segs:
+        return
+    import concurrent.futures as cf
+    pool = _slots(device)
+    nw = min(len(pool), len(segs))
+    streams = [torch.cuda.Stream(device) for _ in range(nw)]
+    cur = torch.cuda.current_stream(device)
+    for st in streams:
+        st.wait_stream(cur)
+
+    def work(w):
+        events = [None, None]
+        with torch.cuda.device(device):
+            for i, (off, dev) in enumerate(segs[w::nw]):
+                k = i & 1
+                if events[k] is not None:
+                    events[k].synchronize()
+                events[k] = fn(pool[w][k], off, dev, streams[w])
+            for e in events:
+                if e is not None:
+                    e.synchronize()
+
+    with cf.ThreadPoolExecutor(nw) as ex:
+        for f in [ex.submit(work, w) for w in range(nw)]:
+            f.result()
+    for st in streams:
+        cur.wait_stream(st)
+
+
+def _prepare(scene):
     dims, k, cols = _columns(scene)
     scene.validate()
     n = scene.count
     header = _HEADER.pack(SCENE_MAGIC, SCENE_VERSION if k == 1 else SCENE_VERSION_SH, dims, n)
     if k != 1:
         header += _SH_FIELD.pack(k)
-    floats = sum(w for _, w in cols)
-    buf, pad = _pinned(len(header) + 4 * n * floats, len(header))
-    buf[pad:pad + len(header)] = torch.frombuffer(bytearray(header), dtype=torch.uint8)
-    body = buf[pad + len(header):].view(torch.float32)
-    off = 0
-    for col, w in cols:
-        body[off:off + n * w].view(n, w).copy_(col.reshape(n, w), non_blocking=True)
-        off += n * w
-    if n:
-        torch.cuda.current_stream(scene.device).synchronize()
-    return buf, pad, buf.numel()
+    dev_cols = [col.reshape(n, w).contiguous() for col, w in cols]
+    segs, end = _segments(dev_cols, len(header))
+    return header, segs, end
+
+
+def _d2h_to(write):
+    def fn(slot, off, dev, stream):
+        view = slot[:dev.numel()]
+        with torch.cuda.stream(stream):
+            view.copy_(dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        ev.synchronize()
+        write(view, off)
+        return None
+    return fn
 
 
 def scene_bytes(scene) -> bytes:
     """The canonical byte string of a scene (io_cli.py:83-89)."""
-    buf, start, end = _pack(scene)
-    return buf[start:end].numpy().tobytes()
+    header, segs, end = _prepare(scene)
+    out = bytearray(end)
+    out[:len(header)] = header
+    mv = memoryview(out)
+
+    def write(view, off):
+        mv[off:off + view.numel()] = view.numpy().data
+
+    _run_chunks(segs, scene.device, _d2h_to(write))
+    return bytes(out)
 
 
 def write_scene(scene, path):
-    """Write a scene atomically: temp file in the target directory, then rename (io_cli.py:60-68,92-93)."""
-    buf, start, end = _pack(scene)
+    """Write a scene atomically: temp file in the target directory, then rename (io_cli.py:60-68,92-93).
+    Chunks are written with parallel pwrite at their final offsets."""
+    header, segs, end = _prepare(scene)
     path = os.fspath(path)
     directory = os.path.dirname(path) or "."
     fd, tmp = tempfile.mkstemp(dir=directory, prefix=".tmp.")
     try:
-        with os.fdopen(fd, "wb") as fh:
-            fh.write(memoryview(buf[start:end].numpy()))
+        os.ftruncate(fd, end)
+        os.pwrite(fd, header, 0)
+
+        def write(view, off):
+            mv = memoryview(view.numpy())
+            done = 0
+            while done < len(mv):
+                done += os.pwrite(fd, mv[done:], off + done)
+
+        _run_chunks(segs, scene.device, _d2h_to(write))
+        os.close(fd)
+        fd = -1
         os.replace(tmp, path)
     except BaseException:
+        if fd >= 0:
+            os.close(fd)
         if os.path.exists(tmp):
             os.unlink(tmp)
         raise
@@ -133,37 +211,31 @@ def read_scene(path, capacity=None, device=None):
     size = os.path.getsize(path)
     with open(path, "rb") as fh:
         head = fh.read(min(size, _HEADER.size + _SH_FIELD.size))
-        if head[:4] != SCENE_MAGIC:
-            if len(head) < 4 and SCENE_MAGIC.startswith(head):
-                raise SizeMismatchError(f"truncated header: {len(head)} bytes")
-            raise BadMagicError(f"bad magic {head[:4]!r}")
-        if len(head) < _HEADER.size:
+    if head[:4] != SCENE_MAGIC:
+        if len(head) < 4 and SCENE_MAGIC.startswith(head):
             raise SizeMismatchError(f"truncated header: {len(head)} bytes")
-        _, version, dims, count = _HEADER.unpack_from(head)
-        if version not in (SCENE_VERSION, SCENE_VERSION_SH):
-            raise UnsupportedVersionError(f"unsupported version {version}")
-        if dims not in RECORD_FLOATS:
-            raise SceneFormatError(f"dims must be 2 or 3, got {dims}")
-        hlen, k = _HEADER.size, 1
-        if version == SCENE_VERSION_SH:
-            if dims != 3 or len(head) < hlen + _SH_FIELD.size:
-                raise SceneFormatError("version 2 needs dims 3 and an SH coefficient count")
-            (k,) = _SH_FIELD.unpack_from(head, hlen)
-            hlen += _SH_FIELD.size
-            if k < 1:
-                raise SceneFormatError("SH coefficient count must be positive")
-        floats = RECORD_FLOATS[dims] + 3 * (k - 1)
-        expected = hlen + count * floats * 4
-        if size != expected:
-            raise SizeMismatchError(
-                f"payload size {size - hlen} does not match "
-                f"count {count} (expected {expected - hlen})")
-        buf, pad = _pinned(size - hlen, 0)
-        fh.seek(hlen)
-        got = fh.readinto(memoryview(buf.numpy())) if count else 0
-        if got != size - hlen:
-            raise SizeMismatchError(f"short read: {got} of {size - hlen} payload bytes")
-    body = buf.view(torch.float32)
+        raise BadMagicError(f"bad magic {head[:4]!r}")
+    if len(head) < _HEADER.size:
+        raise SizeMismatchError(f"truncated header: {len(head)} bytes")
+    _, version, dims, count = _HEADER.unpack_from(head)
+    if version not in (SCENE_VERSION, SCENE_VERSION_SH):
+        raise UnsupportedVersionError(f"unsupported version {version}")
+    if dims not in RECORD_FLOATS:
+        raise SceneFormatError(f"dims must be 2 or 3, got {dims}")
+    hlen, k = _HEADER.size, 1
+    if version == SCENE_VERSION_SH:
+        if dims != 3 or len(head) < hlen + _SH_FIELD.size:
+            raise SceneFormatError("version 2 needs dims 3 and an SH coefficient count")
+        (k,) = _SH_FIELD.unpack_from(head, hlen)
+        hlen += _SH_FIELD.size
+        if k < 1:
+            raise SceneFormatError("SH coefficient count must be positive")
+    floats = RECORD_FLOATS[dims] + 3 * (k - 1)
+    expected = hlen + count * floats * 4
+    if size != expected:
+        raise SizeMismatchError(
+            f"payload size {size - hlen} does not match "
+            f"count {count} (expected {expected - hlen})")
     n = int(count)
     cap = max(n, 1) if capacity is None else int(capacity)
     if cap < n:
@@ -179,10 +251,27 @@ def read_scene(path, capacity=None, device=None):
         c = scene._cols
         dst = [(c["positions"], 2), (c["log_scales"], 2), (c["thetas"], 1),
                (c["opacity_logits"], 1), (c["colors"], 3)]
-    off = 0
-    for col, w in dst:
-        col.view(cap, w)[:n].copy_(body[off:off + n * w].view(n, w), non_blocking=True)
-        off += n * w
+    segs, _ = _segments([col.view(cap, w)[:n] for col, w in dst], hlen)
+    fd = os.open(path, os.O_RDONLY)
+    try:
+        def fn(slot, off, devb, stream):
+            view = slot[:devb.numel()]
+            mv = memoryview(view.numpy())
+            got = 0
+            while got < len(mv):
+                r = os.preadv(fd, [mv[got:]], off + got)
+                if r <= 0:
+                    raise SizeMismatchError(f"short read at byte {off + got}")
+                got += r
+            with torch.cuda.stream(stream):
+                devb.copy_(view, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+            return ev
+
+        _run_chunks(segs, dev, fn)
+    finally:
+        os.close(fd)
     if dims == 3 and n:
         L = _lib.lib()
         flags = torch.empty(1, dtype=torch.int32, device=dev)
