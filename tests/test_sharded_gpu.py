@@ -73,13 +73,14 @@ def _cloud(n, seed):
     return random_cloud(n, 16, seed=seed)
 
 
-def _worker(rank, world, port, n, q):
+def _worker(rank, world, port, n, q, backend="gloo"):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group(backend, rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0) if backend == "nccl" else None)
     try:
         import paper_2603_08661_b200 as b
         from paper_2603_08661_b200 import sharded
@@ -99,7 +100,10 @@ def _worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-def test_world2_gloo_densify_step_matches_single_device():
+@pytest.mark.parametrize("world,backend", [(2, "gloo"), (1, "nccl")])
+def test_sharded_densify_step_matches_single_device(world, backend):
+    """world 2 over gloo (two ranks on the one GPU), and world 1 over NCCL (the production
+    backend's collectives on device buffers)."""
     import paper_2603_08661_b200 as b
     n = 20_001
     pos, ls, qq, o, sh = _cloud(n, 11)
@@ -113,7 +117,8 @@ def test_world2_gloo_densify_step_matches_single_device():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, backend))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
