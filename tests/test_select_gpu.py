@@ -149,11 +149,12 @@ def test_hypot_bit_exact_wide_range():
     b = B()
     rng = np.random.default_rng(77)
     n = 1 << 22
-    g = rng.standard_normal((n, 2)) * np.exp2(rng.integers(-1074, 1023, (n, 2)).clip(-1070, 1000))
-    g[::7, 1] = 0.0
-    g[::11, 0] = -0.0
-    g[::13] = g[::13] * np.exp2(rng.integers(-60, 60, (len(g[::13]), 1)))  # near-equal and far
-    g[1::17, 1] = g[1::17, 0] * rng.uniform(0.999, 1.001, len(g[1::17]))
+    with np.errstate(over="ignore"):
+        g = rng.standard_normal((n, 2)) * np.exp2(rng.integers(-1074, 1023, (n, 2)).clip(-1070, 1000))
+        g[::7, 1] = 0.0
+        g[::11, 0] = -0.0
+        g[::13] = g[::13] * np.exp2(rng.integers(-60, 60, (len(g[::13]), 1)))  # near-equal and far
+        g[1::17, 1] = g[1::17, 0] * rng.uniform(0.999, 1.001, len(g[1::17]))
     sp = np.array([[np.inf, 1.0], [np.nan, np.inf], [np.nan, 1.0], [5e-324, 0.0], [0.0, 0.0],
                    [1.7976931348623157e308, 1.7976931348623157e308], [3.0, 4.0], [1e-300, 1e-310]])
     g[:len(sp)] = sp
