@@ -27,8 +27,10 @@ namespace igs {
 namespace las {
 
 constexpr int NT = 256;
-constexpr int PER = 4;
+constexpr int PER = 2;
 constexpr int TILE = NT * PER;  // Gaussians per block
+constexpr int SUBS = PER * NT / 32;  // (sub-tile, warp) ballot groups per tile
+static_assert(SUBS <= 32, "one warp scans the tile");
 
 struct Layout {
   size_t tile_cnt, tile_off, total;
@@ -166,18 +168,17 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
   }
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan over (sub-tile, warp) in index order
-    unsigned v = warp_cnt[threadIdx.x];
+    unsigned v = threadIdx.x < (unsigned)SUBS ? warp_cnt[threadIdx.x] : 0u;
     unsigned x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       unsigned y = __shfl_up_sync(0xffffffffu, x, o);
       if (threadIdx.x >= (unsigned)o) x += y;
     }
-    warp_pre[threadIdx.x] = x - v;
+    if (threadIdx.x < (unsigned)SUBS) warp_pre[threadIdx.x] = x - v;
     if (threadIdx.x == 31) s_total = x;
   }
   __syncthreads();
-  static_assert(PER * NT / 32 == 32, "one warp scans the tile");
   const unsigned long long slot0 = (unsigned long long)count + tile_off[blockIdx.x];
 
 #pragma unroll
@@ -295,14 +296,14 @@ __global__ void __launch_bounds__(NT) las2d_apply_kernel(
   }
   __syncthreads();
   if (threadIdx.x < 32) {
-    unsigned v = warp_cnt[threadIdx.x];
+    unsigned v = threadIdx.x < (unsigned)SUBS ? warp_cnt[threadIdx.x] : 0u;
     unsigned x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       unsigned y = __shfl_up_sync(0xffffffffu, x, o);
       if (threadIdx.x >= (unsigned)o) x += y;
     }
-    warp_pre[threadIdx.x] = x - v;
+    if (threadIdx.x < (unsigned)SUBS) warp_pre[threadIdx.x] = x - v;
   }
   __syncthreads();
   const unsigned long long slot0 = (unsigned long long)count + tile_off[blockIdx.x];
