@@ -181,6 +181,21 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
   __syncthreads();
   const unsigned long long slot0 = (unsigned long long)count + tile_off[blockIdx.x];
 
+  // every load of the thread's parents first (one memory latency), then the arithmetic
+  float lv[PER][3], pv[PER][3], ov[PER];
+  float4 qv[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    if (!m[j]) continue;
+    const long long i = base + j * NT + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lv[j][k] = ls[3 * i + k];
+      pv[j][k] = pos[3 * i + k];
+    }
+    ov[j] = opac[i];
+    qv[j] = reinterpret_cast<const float4*>(rot)[i];
+  }
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     if (!m[j]) continue;
@@ -190,7 +205,7 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
     src_idx[r] = i;
 
     // _split_common (las_split.py:78-99)
-    float l0 = ls[3 * i], l1 = ls[3 * i + 1], l2 = ls[3 * i + 2];
+    const float l0 = lv[j][0], l1 = lv[j][1], l2 = lv[j][2];
     int l = 0;  // np.argmax: first maximum (a NaN counts as the maximum)
     float best = l0;
     if (!(best != best)) {
@@ -201,11 +216,11 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
     float cl0 = l0 + c.log_gamma, cl1 = l1 + c.log_gamma, cl2 = l2 + c.log_gamma;
     const float cll = best + c.log_alpha;
     if (l == 0) cl0 = cll; else if (l == 1) cl1 = cll; else cl2 = cll;
-    const float raw = raw_opacity(opac[i], c.beta);
+    const float raw = raw_opacity(ov[j], c.beta);
     const float co = logf(raw / (1.0f - raw));
 
     // quat_to_rotmat (core.py:32-58), column l only (axis_displacement, las_split.py:62-75)
-    float4 q = reinterpret_cast<const float4*>(rot)[i];
+    const float4 q = qv[j];
     float w = q.x, x = q.y, y = q.z, z = q.w;
     if (renorm) {
       float n = quat_norm(q);
@@ -226,7 +241,7 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
       c2 = 1.0f - 2.0f * (x * x + y * y);
     }
     const float d0 = c0 * offset, d1 = c1 * offset, d2 = c2 * offset;
-    const float p0 = pos[3 * i], p1 = pos[3 * i + 1], p2 = pos[3 * i + 2];
+    const float p0 = pv[j][0], p1 = pv[j][1], p2 = pv[j][2];
 
     // parent slot <- +offset child
     pos[3 * i] = p0 + d0;
