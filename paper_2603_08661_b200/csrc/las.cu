@@ -70,20 +70,33 @@ __global__ void __launch_bounds__(NT) las_prepare_kernel(const uint8_t* __restri
   __shared__ unsigned warp_cnt[NT / 32];
   const long long base = (long long)blockIdx.x * TILE;
   unsigned local = 0, flags = 0;
+  bool m[PER];
+  float4 q[PER];
+  float o[PER];
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    long long i = base + j * NT + threadIdx.x;
-    if (i < count && mask[i]) {
-      ++local;
-      if (rot) {  // 3-D scenes: quaternion checks (2-D scenes pass rot = nullptr)
-        float4 q = reinterpret_cast<const float4*>(rot)[i];
-        float n = quat_norm(q);
-        if (!isfinite(n) || n == 0.0f) flags |= IGS_LAS_BAD_QUAT;
-        else if (fabsf(n - 1.0f) > 1e-4f) flags |= IGS_LAS_RENORM;
-      }
-      float r = raw_opacity(opac[i], beta);
-      if (!(r > 0.0f && r < 1.0f)) flags |= IGS_LAS_BAD_OPACITY;
+    const long long i = base + j * NT + threadIdx.x;
+    m[j] = i < count && mask[i];
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {  // every load first, then the checks
+    const long long i = base + j * NT + threadIdx.x;
+    if (m[j]) {
+      if (rot) q[j] = reinterpret_cast<const float4*>(rot)[i];
+      o[j] = opac[i];
     }
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    if (!m[j]) continue;
+    ++local;
+    if (rot) {  // 3-D scenes: quaternion checks (2-D scenes pass rot = nullptr)
+      float n = quat_norm(q[j]);
+      if (!isfinite(n) || n == 0.0f) flags |= IGS_LAS_BAD_QUAT;
+      else if (fabsf(n - 1.0f) > 1e-4f) flags |= IGS_LAS_RENORM;
+    }
+    float r = raw_opacity(o[j], beta);
+    if (!(r > 0.0f && r < 1.0f)) flags |= IGS_LAS_BAD_OPACITY;
   }
   unsigned w = __reduce_add_sync(0xffffffffu, local);
   unsigned f = __reduce_or_sync(0xffffffffu, flags);
