@@ -373,25 +373,21 @@ def bench_las(args, world, dev, peak, peak_src):
             getattr(scene, k)[:n].copy_(v[:n])
         scene._set_count(n)
 
-    # all-masked LAS through the public call (prepare + 16-byte D2H + apply)
-    times, kern = [], []
+    # all-masked LAS through the public call: las_split_batch = fused pre-pass + device-guarded
+    # apply, then the 16-byte summary read
+    times = []
     steps = max(3, min(args.steps, 20))
     for it in range(args.warmup + steps):
         restore()
         torch.cuda.synchronize()
-        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        prep = igs.las_split.prepare(scene, mask, igs.SplitConstants())
-        ns, fl = (int(v) for v in prep.summary.cpu())
-        b.record()
-        igs.las_split.check_and_apply(prep, ns, fl, igs.SplitConstants())
+        igs.las_split_batch(scene, mask)
         c.record()
         torch.cuda.synchronize()
         if it >= args.warmup:
             times.append(a.elapsed_time(c))
-            kern.append(b.elapsed_time(c))
     ms = max_over_ranks(statistics.median(times), world)
-    ms_apply = max_over_ranks(statistics.median(kern), world)
     # the apply kernel alone: K back-to-back launches on one prepared workspace between two
     # events (each launch moves the same bytes; the scene is restored afterwards), so the
     # per-launch time excludes the host's launch gap that the public-call timing above sees
@@ -446,11 +442,9 @@ def bench_las(args, world, dev, peak, peak_src):
                         "unit": "GB/s", "frac": round(achieved / peak, 4),
                         "traffic": (round(las_traffic * n) if las_traffic else None),
                         "kernel": "las_apply_kernel", "algorithmic_bytes_per_split": 500,
-                        "kernel_ms": round(ms_kernel, 4),
-                        "apply_ms": round(ms_apply, 4), "peak_source": peak_src,
+                        "kernel_ms": round(ms_kernel, 4), "peak_source": peak_src,
                         "timing": "kernel_ms: 10 back-to-back apply launches between CUDA "
-                                  "events; apply_ms: the public check_and_apply call incl. "
-                                  "its host launch gap"},
+                                  "events; ms_per_step: the public las_split_batch call"},
            "densify_step": {"ms": round(ds_ms, 4), "n": n, "split": ev.split,
                             "eligible": ev.eligible,
                             "note": "select (radix top-k, take=ceil(0.05 N)) + LAS + one host "

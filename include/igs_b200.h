@@ -182,6 +182,16 @@ int igs_las_apply(float* positions, float* log_scales, float* rotations, float* 
                   float beta, int renormalize, void* workspace, size_t workspace_bytes,
                   void* stream);
 
+/* The whole split in one call, no host round trip between the passes: igs_las_prepare, then
+ * the apply pass guarded on the device by the summary it wrote.  If count + n_split >
+ * capacity or a domain flag (BAD_QUAT / BAD_OPACITY) is set, nothing in the scene is written;
+ * the caller reads summary {n_split, flags} afterwards and raises (BudgetError / ValueError)
+ * or adds n_split to its count.  Renormalisation follows the summary's RENORM flag. */
+int igs_las_split(float* positions, float* log_scales, float* rotations, float* opacity_logits,
+                  float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
+                  const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,
+                  void* workspace, size_t workspace_bytes, int64_t* summary, void* stream);
+
 /* 2-D Long-Axis-Split (las_split.py:182-197), after igs_las_prepare with rotations = NULL
  * (no quaternion checks).  Columns: positions (cap,2), log_scales (cap,2), thetas (cap,),
  * opacity_logits (cap,), colors (cap,3), float32; the same slot rule as igs_las_apply. */
@@ -189,6 +199,12 @@ int igs_las2d_apply(float* positions, float* log_scales, float* thetas, float* o
                     float* colors, int64_t count, int64_t capacity, const uint8_t* mask,
                     float alpha, float log_alpha, float log_gamma, float beta, void* workspace,
                     size_t workspace_bytes, void* stream);
+
+/* igs_las_split for a 2-D scene (las_split.py:182-197): same guard (BAD_OPACITY only). */
+int igs_las2d_split(float* positions, float* log_scales, float* thetas, float* opacity_logits,
+                    float* colors, int64_t count, int64_t capacity, const uint8_t* mask,
+                    float alpha, float log_alpha, float log_gamma, float beta, void* workspace,
+                    size_t workspace_bytes, int64_t* summary, void* stream);
 
 /* ---- scene files (io_cli.py:83-134) ------------------------------------- */
 

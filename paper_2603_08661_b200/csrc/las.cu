@@ -154,6 +154,16 @@ __device__ __forceinline__ void clone_rows(float* sh, const long long* src_idx, 
   }
 }
 
+// Fused split (igs_las_split / igs_las2d_split): the apply pass runs right behind the
+// pre-pass and reads its summary {n_split, flags} itself; any error the host will raise
+// (BudgetError, or a flagged domain error) makes every block return before writing, so the
+// scene is untouched exactly as when the host checks first.
+__device__ __forceinline__ bool split_guard(const unsigned long long* guard, long long count,
+                                            long long capacity, unsigned long long bad) {
+  const unsigned long long ns = guard[0], fl = guard[1];
+  return ns != 0 && (unsigned long long)count + ns <= (unsigned long long)capacity && !(fl & bad);
+}
+
 struct Consts {
   float alpha, log_alpha, log_gamma, beta;
 };
@@ -162,10 +172,15 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
     float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ rot,
     float* __restrict__ opac, float* __restrict__ sh, long long sh_floats, long long count,
     const uint8_t* __restrict__ mask, Consts c, int renorm,
-    const unsigned long long* __restrict__ tile_off) {
+    const unsigned long long* __restrict__ tile_off, const unsigned long long* guard,
+    long long capacity) {
   __shared__ unsigned warp_cnt[PER * NT / 32];
   __shared__ unsigned warp_pre[PER * NT / 32];
   __shared__ long long src_idx[TILE];
+  if (guard) {  // fused split: the pre-pass summary decides on the device (see split_guard)
+    if (!split_guard(guard, count, capacity, IGS_LAS_BAD_QUAT | IGS_LAS_BAD_OPACITY)) return;
+    renorm = (guard[1] & IGS_LAS_RENORM) != 0;
+  }
   __shared__ unsigned s_total;
   const long long base = (long long)blockIdx.x * TILE;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -307,9 +322,11 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
 __global__ void __launch_bounds__(NT) las2d_apply_kernel(
     float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ theta,
     float* __restrict__ opac, float* __restrict__ col, long long count,
-    const uint8_t* __restrict__ mask, Consts c, const unsigned long long* __restrict__ tile_off) {
+    const uint8_t* __restrict__ mask, Consts c, const unsigned long long* __restrict__ tile_off,
+    const unsigned long long* guard, long long capacity) {
   __shared__ unsigned warp_cnt[PER * NT / 32];
   __shared__ unsigned warp_pre[PER * NT / 32];
+  if (guard && !split_guard(guard, count, capacity, IGS_LAS_BAD_OPACITY)) return;
   const long long base = (long long)blockIdx.x * TILE;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   bool m[PER];
@@ -427,7 +444,7 @@ int igs_las_apply(float* positions, float* log_scales, float* rotations, float* 
   las::Consts c{alpha, log_alpha, log_gamma, beta};
   las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
       positions, log_scales, rotations, opacity_logits, sh, sh_floats, count, mask, c,
-      renormalize, (const unsigned long long*)((char*)workspace + L.tile_off));
+      renormalize, (const unsigned long long*)((char*)workspace + L.tile_off), nullptr, 0);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }
@@ -446,7 +463,52 @@ int igs_las2d_apply(float* positions, float* log_scales, float* thetas, float* o
   las::Consts c{alpha, log_alpha, log_gamma, beta};
   las::las2d_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
       positions, log_scales, thetas, opacity_logits, colors, count, mask, c,
-      (const unsigned long long*)((char*)workspace + L.tile_off));
+      (const unsigned long long*)((char*)workspace + L.tile_off), nullptr, 0);
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
+int igs_las_split(float* positions, float* log_scales, float* rotations, float* opacity_logits,
+                  float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
+                  const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,
+                  void* workspace, size_t workspace_bytes, int64_t* summary, void* stream) {
+  if (count < 0 || capacity < count || sh_floats < 0) return IGS_ERR_ARGUMENT;
+  if (count > 0 && (!positions || !log_scales || !rotations || !opacity_logits))
+    return IGS_ERR_ARGUMENT;
+  if (sh_floats > 0 && count > 0 && !sh) return IGS_ERR_ARGUMENT;
+  if (((uintptr_t)rotations & 15) || (sh_floats % 4 == 0 && ((uintptr_t)sh & 15)))
+    return IGS_ERR_ARGUMENT;
+  int st = igs_las_prepare(mask, rotations, opacity_logits, count, beta, workspace,
+                           workspace_bytes, summary, stream);
+  if (st != IGS_OK || count == 0) return st;
+  las::Layout L = las::layout(count);
+  long long tiles = (count + las::TILE - 1) / las::TILE;
+  las::Consts c{alpha, log_alpha, log_gamma, beta};
+  las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
+      positions, log_scales, rotations, opacity_logits, sh, sh_floats, count, mask, c, 0,
+      (const unsigned long long*)((char*)workspace + L.tile_off),
+      (const unsigned long long*)summary, capacity);
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
+int igs_las2d_split(float* positions, float* log_scales, float* thetas, float* opacity_logits,
+                    float* colors, int64_t count, int64_t capacity, const uint8_t* mask,
+                    float alpha, float log_alpha, float log_gamma, float beta, void* workspace,
+                    size_t workspace_bytes, int64_t* summary, void* stream) {
+  if (count < 0 || capacity < count) return IGS_ERR_ARGUMENT;
+  if (count > 0 && (!positions || !log_scales || !thetas || !opacity_logits || !colors))
+    return IGS_ERR_ARGUMENT;
+  int st = igs_las_prepare(mask, nullptr, opacity_logits, count, beta, workspace,
+                           workspace_bytes, summary, stream);
+  if (st != IGS_OK || count == 0) return st;
+  las::Layout L = las::layout(count);
+  long long tiles = (count + las::TILE - 1) / las::TILE;
+  las::Consts c{alpha, log_alpha, log_gamma, beta};
+  las::las2d_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
+      positions, log_scales, thetas, opacity_logits, colors, count, mask, c,
+      (const unsigned long long*)((char*)workspace + L.tile_off),
+      (const unsigned long long*)summary, capacity);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }

@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from . import las_split as _las
-from .core import Scene3
+from .core import Scene2, Scene3
 from .schedule import DensifyConfig, is_densify_step, is_warmup_step
 
 
@@ -156,18 +156,18 @@ def densify_step(scene, stats: DensifyStats, cfg: DensifyConfig, step: int) -> D
         raise ValueError(f"step {step} is not a densify step for this timetable")
     if len(stats) != scene.count:
         raise ValueError("stats length does not match scene count")
-    if not isinstance(scene, Scene3):
-        # Scene2 (2-D desk-scale harness) is out of scope for the B200 path
+    if not isinstance(scene, (Scene2, Scene3)):
         raise TypeError(f"unsupported scene type {type(scene).__name__}")
     headroom = scene.capacity - scene.count
     n = scene.count
     take_cap = _take_cap(cfg, n, headroom) if (headroom > 0 and n > 0) else 0
     c = cfg.split_constants
     if take_cap > 0:
+        # select, then the fused split (pre-pass + device-guarded apply); one host read
         mask, counts = _launch_select(stats, cfg, step, take_cap)
-        prep = _las.prepare(scene, mask.view(torch.bool), c)
-        eligible, _, n_split, flags = (int(v) for v in torch.cat([counts, prep.summary]).cpu())
-        _las.check_and_apply(prep, n_split, flags, c)
+        summary = _las.split_async(scene, mask.view(torch.bool), c)
+        eligible, _, n_split, flags = (int(v) for v in torch.cat([counts, summary]).cpu())
+        _las.finish_split(scene, n_split, flags)
     else:
         eligible, n_split = eligible_count(stats, cfg, step), 0
     stats.reset(scene.count)

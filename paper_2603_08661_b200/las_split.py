@@ -107,13 +107,57 @@ def check_and_apply(prep: _Prepared, n_split: int, flags: int, c: SplitConstants
     return scene.count
 
 
+def split_async(scene, mask, c: SplitConstants):
+    """Launch the fused split (igs_las_split / igs_las2d_split): the pre-pass, then the apply
+    pass guarded on the device by the pre-pass summary, with no host round trip between them.
+    Returns the summary (device int64[2] = {n_split, flags}), not yet read."""
+    L = _lib.lib()
+    m = _mask_tensor(mask, scene.count, scene.device)
+    nbytes = _lib.query_size(L.igs_las_workspace_bytes, scene.count)
+    ws = _lib.workspace(nbytes, scene.device, "las")
+    summary = torch.empty(2, dtype=torch.int64, device=scene.device)
+    alpha, log_alpha, log_gamma, beta = c.device_constants()
+    if isinstance(scene, Scene3):
+        _lib.check(L.igs_las_split(scene._pos.data_ptr(), scene._ls.data_ptr(),
+                                   scene._rot.data_ptr(), scene._op.data_ptr(),
+                                   scene._sh.data_ptr(), scene._sh.shape[1] * 3, scene.count,
+                                   scene.capacity, m.data_ptr(), alpha, log_alpha, log_gamma,
+                                   beta, ws.data_ptr(), ws.numel(), summary.data_ptr(),
+                                   _lib.stream_handle()), "las_split_batch")
+    else:
+        cols = scene._cols
+        _lib.check(L.igs_las2d_split(cols["positions"].data_ptr(), cols["log_scales"].data_ptr(),
+                                     cols["thetas"].data_ptr(), cols["opacity_logits"].data_ptr(),
+                                     cols["colors"].data_ptr(), scene.count, scene.capacity,
+                                     m.data_ptr(), alpha, log_alpha, log_gamma, beta,
+                                     ws.data_ptr(), ws.numel(), summary.data_ptr(),
+                                     _lib.stream_handle()), "las_split_batch_2d")
+    return summary
+
+
+def finish_split(scene, n_split: int, flags: int):
+    """Host half of the fused split: the reference's errors in its order (las_split.py:158-179;
+    the device left the scene untouched in every error case), else the grown count."""
+    if scene.count + n_split > scene.capacity:
+        raise BudgetError(f"splitting {n_split} of {scene.count} primitives exceeds "
+                          f"capacity {scene.capacity}")
+    if n_split == 0:
+        return scene.count
+    if flags & _lib.IGS_LAS_BAD_OPACITY:
+        raise ValueError("logit requires all values strictly inside (0, 1)")
+    if flags & _lib.IGS_LAS_BAD_QUAT:
+        raise ValueError("zero or non-finite quaternion")
+    scene._set_count(scene.count + n_split)
+    return scene.count
+
+
 def las_split_batch(scene: Scene3, mask, c: SplitConstants = SplitConstants()) -> Scene3:
     """Split every masked primitive of a GPU scene in place (las_split.py:158-179)."""
     if not isinstance(scene, Scene3):
         raise TypeError(f"expected a paper_2603_08661_b200.core.Scene3, got {type(scene).__name__}")
-    prep = prepare(scene, mask, c)
-    n_split, flags = (int(v) for v in prep.summary.cpu().tolist())
-    check_and_apply(prep, n_split, flags, c)
+    summary = split_async(scene, mask, c)
+    n_split, flags = (int(v) for v in summary.cpu().tolist())
+    finish_split(scene, n_split, flags)
     return scene.validate()
 
 
@@ -129,28 +173,7 @@ def las_split_batch_2d(scene: Scene2, mask, c: SplitConstants = SplitConstants()
     parents take the +offset child in place, -offset children are appended in parent order."""
     if not isinstance(scene, Scene2):
         raise TypeError(f"expected a paper_2603_08661_b200.core.Scene2, got {type(scene).__name__}")
-    L = _lib.lib()
-    m = _mask_tensor(mask, scene.count, scene.device)
-    nbytes = _lib.query_size(L.igs_las_workspace_bytes, scene.count)
-    ws = _lib.workspace(nbytes, scene.device, "las")
-    summary = torch.empty(2, dtype=torch.int64, device=scene.device)
-    alpha, log_alpha, log_gamma, beta = c.device_constants()
-    cols = scene._cols
-    _lib.check(L.igs_las_prepare(m.data_ptr(), None, cols["opacity_logits"].data_ptr(),
-                                 scene.count, beta, ws.data_ptr(), ws.numel(),
-                                 summary.data_ptr(), _lib.stream_handle()), "las_split_batch_2d")
+    summary = split_async(scene, mask, c)
     n_split, flags = (int(v) for v in summary.cpu().tolist())
-    if scene.count + n_split > scene.capacity:
-        raise BudgetError(f"splitting {n_split} of {scene.count} primitives exceeds "
-                          f"capacity {scene.capacity}")
-    if n_split == 0:
-        return scene
-    if flags & _lib.IGS_LAS_BAD_OPACITY:
-        raise ValueError("logit requires all values strictly inside (0, 1)")
-    _lib.check(L.igs_las2d_apply(cols["positions"].data_ptr(), cols["log_scales"].data_ptr(),
-                                 cols["thetas"].data_ptr(), cols["opacity_logits"].data_ptr(),
-                                 cols["colors"].data_ptr(), scene.count, scene.capacity,
-                                 m.data_ptr(), alpha, log_alpha, log_gamma, beta, ws.data_ptr(),
-                                 ws.numel(), _lib.stream_handle()), "las_split_batch_2d")
-    scene._set_count(scene.count + n_split)
+    finish_split(scene, n_split, flags)
     return scene.validate()

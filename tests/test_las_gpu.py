@@ -196,3 +196,60 @@ def test_las2d_errors():
     assert sc.count == 4
     b.las_split_batch_2d(sc, np.zeros(4, bool))
     assert sc.count == 4
+
+
+def test_densify_step_scene2_matches_oracle():
+    """densify_step on a 2-D scene (densify_controller.py:125-147 dispatches to
+    las_split_batch_2d): the fused select + guarded 2-D split against the oracle."""
+    from oracle import select as OS
+    b = B()
+    rng = np.random.default_rng(8)
+    n = 5000
+    cols = {"positions": rng.normal(size=(n, 2)), "log_scales": rng.uniform(-0.7, 0.7, (n, 2)),
+            "thetas": rng.uniform(-np.pi, np.pi, n), "opacity_logits": rng.normal(0, 1.5, n),
+            "colors": rng.random((n, 3))}
+    cols = {k: v.astype(np.float32) for k, v in cols.items()}
+    sc = b.Scene2(cols["positions"], cols["log_scales"], cols["thetas"], cols["opacity_logits"],
+                  cols["colors"], capacity=n + 600)
+    grad, edge = rng.exponential(3e-4, n), rng.random(n)
+    st = b.DensifyStats(n)
+    b.accumulate_grads(st, grad)
+    st.set_edge_score(edge)
+    cfg = b.DensifyConfig(budget=n + 600)
+    ev = b.densify_step(sc, st, cfg, 2000)
+    mask, elig = OS.select_candidates(grad, edge, False, "product", cfg.grad_threshold,
+                                      cfg.growth_cap, 600)
+    assert (ev.eligible, ev.split, ev.count_after) == (elig, int(mask.sum()), n + int(mask.sum()))
+    k = cfg.split_constants
+    want = OL.las_split_batch_2d(dict(cols, capacity=n + 600), mask, k.alpha, k.gamma_axis, k.beta)
+    got = sc.to_numpy()
+    for c in ("log_scales", "thetas", "colors"):
+        assert_array_equal(got[c], want[c], err_msg=c)
+    wp = want["positions"].astype(np.float64)
+    assert (np.abs(got["positions"] - wp) <= 1e-5 * (np.abs(wp) + 1.0)).all()
+    wo = want["opacity_logits"]
+    assert (np.abs(got["opacity_logits"] - wo) <= 1e-5 * np.maximum(1.0, np.abs(wo))).all()
+    assert len(st) == sc.count
+
+
+def test_fused_split_leaves_scene_untouched_on_errors():
+    """igs_las_split decides on the device: BudgetError and the logit-domain ValueError leave
+    every column as it was (las_split.py:158-179 raise before mutating)."""
+    b = B()
+    n = 64
+    q = np.tile([1.0, 0, 0, 0], (n, 1))
+    sc = b.Scene3(np.arange(3 * n).reshape(n, 3), np.zeros((n, 3)), q, np.zeros(n),
+                  np.ones((n, 3)), capacity=n + 10)
+    before = sc.to_numpy()
+    with pytest.raises(b.BudgetError):
+        b.las_split_batch(sc, np.ones(n, bool))
+    sc2 = b.Scene3(np.arange(3 * n).reshape(n, 3), np.zeros((n, 3)), q, np.full(n, 1e9),
+                   np.ones((n, 3)), capacity=2 * n)
+    before2 = sc2.to_numpy()
+    with pytest.raises(ValueError):
+        b.las_split_batch(sc2, np.ones(n, bool), b.SplitConstants(beta=1.0))
+    for s_, bf in ((sc, before), (sc2, before2)):
+        after = s_.to_numpy()
+        assert s_.count == n
+        for col in ("positions", "log_scales", "rotations", "opacity_logits", "sh"):
+            assert_array_equal(after[col], bf[col])
