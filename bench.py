@@ -300,7 +300,13 @@ def run_ours(args, world, rank, local):
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": (round(traffic * VIEWS * PX) if traffic else None),
                      "kernel": "edge_persistent_kernel", "algorithmic_bytes_per_px": 32,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     "frac_datasheet_8TBps": round(achieved / 8000.0, 4),
+                     "fp64_pipe_active_pct": ncu_traffic().get("edge_fp64_pipe_active_pct"),
+                     "issue_active_pct": ncu_traffic().get("edge_issue_active_pct"),
+                     "note": "the kernel is issue/latency-bound (FP64 blur + integer NMS work); "
+                             "fp64 / issue figures from the committed ncu --set full capture"},
+        "per_gpu_value": round(value / world, 3),
         "clocks": clk.summary(),
         "gpu_launches": args.steps,
     }
