@@ -31,6 +31,7 @@ namespace shard {
 constexpr int NT = 1024;
 constexpr int NBINS = 1 << 16;
 constexpr int ROUNDS = 4;
+constexpr int U = 4;                          // elements per thread per streaming step
 constexpr unsigned long long kIneligible = ~0ull;
 constexpr long long MAX_PER_BLOCK = 65535;   // 16-bit packed shared-memory counters
 constexpr int SMEM_BYTES = NBINS * 2;        // two 16-bit bins per 32-bit word
@@ -117,18 +118,32 @@ __global__ void __launch_bounds__(NT) keys_kernel(KeyParams P) {
   long long lo, hi;
   block_range(P.n, lo, hi);
   unsigned elig = 0;
-  for (long long i = lo + threadIdx.x; i < hi; i += NT) {
-    const double g = P.accum ? P.grad_sum[i] / (double)P.accum : 0.0;
-    const bool e = P.warmup || g > P.thr;
-    double sc;
-    if (P.warmup || P.policy == IGS_POLICY_EDGE) sc = P.edge[i];
-    else if (P.policy == IGS_POLICY_GRAD) sc = g;
-    else sc = P.edge[i] * g;
-    const unsigned long long k = e ? score_key(sc) : kIneligible;
-    P.keys[i] = k;
-    if (e) {
-      ++elig;
-      smem_hist_add(h, (unsigned)(k >> 48));
+  const bool need_edge = P.warmup || P.policy != IGS_POLICY_GRAD;
+  // U elements per thread per step, every load issued before the arithmetic
+  for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
+    double gs[U], ed[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * NT;
+      gs[u] = i < hi ? __ldcs(P.grad_sum + i) : 0.0;
+      ed[u] = (i < hi && need_edge) ? __ldcs(P.edge + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * NT;
+      if (i >= hi) break;
+      const double g = P.accum ? gs[u] / (double)P.accum : 0.0;
+      const bool e = P.warmup || g > P.thr;
+      double sc;
+      if (P.warmup || P.policy == IGS_POLICY_EDGE) sc = ed[u];
+      else if (P.policy == IGS_POLICY_GRAD) sc = g;
+      else sc = ed[u] * g;
+      const unsigned long long k = e ? score_key(sc) : kIneligible;
+      P.keys[i] = k;
+      if (e) {
+        ++elig;
+        smem_hist_add(h, (unsigned)(k >> 48));
+      }
     }
   }
   elig = __reduce_add_sync(0xffffffffu, elig);
@@ -147,9 +162,16 @@ __global__ void __launch_bounds__(NT) hist_kernel(const unsigned long long* __re
   const int sh = round_shift(round);
   long long lo, hi;
   block_range(n, lo, hi);
-  for (long long i = lo + threadIdx.x; i < hi; i += NT) {
-    const unsigned long long k = keys[i];
-    if (k != kIneligible && (k & pmask) == prefix) smem_hist_add(h, (unsigned)((k >> sh) & 0xffffu));
+  for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
+    unsigned long long kv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) kv[u] = i0 + u * NT < hi ? keys[i0 + u * NT] : kIneligible;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned long long k = kv[u];
+      if (k != kIneligible && (k & pmask) == prefix)
+        smem_hist_add(h, (unsigned)((k >> sh) & 0xffffu));
+    }
   }
   smem_hist_flush(h, hist);
 }
@@ -259,7 +281,13 @@ __global__ void __launch_bounds__(NT) ties_kernel(const unsigned long long* __re
   block_range(n, lo, hi);
   unsigned c = 0;
   if (!status)
-    for (long long i = lo + threadIdx.x; i < hi; i += NT) c += (keys[i] == T);
+    for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
+      unsigned long long kv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) kv[u] = i0 + u * NT < hi ? keys[i0 + u * NT] : ~T;
+#pragma unroll
+      for (int u = 0; u < U; ++u) c += (kv[u] == T);
+    }
   c = __reduce_add_sync(0xffffffffu, c);
   if (lane_id() == 0 && c) atomicAdd(&s_cnt, c);
   __syncthreads();
@@ -293,14 +321,33 @@ __global__ void __launch_bounds__(NT) finalize_kernel(const unsigned long long* 
   if (lane_id() == 0 && b) atomicAdd(&s_before, b);
   __syncthreads();
   unsigned long long run = s_before;
-  for (long long c0 = lo; c0 < hi; c0 += NT) {
-    const long long i = c0 + threadIdx.x;
-    const unsigned long long k = i < hi ? keys[i] : kIneligible;
-    const unsigned is_tie = k == T ? 1u : 0u;
-    unsigned tot;
-    const unsigned ex = block_exclusive_scan(is_tie, warp_sums, &tot);
-    if (i < hi) mask[i] = (k < T) || (is_tie && run + ex < need);
-    run += tot;
+  // U-element steps; the tie scan (in index order) only runs for steps that hold a tie
+  for (long long c0 = lo; c0 < hi; c0 += U * NT) {
+    unsigned long long kv[U];
+    int any = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = c0 + u * NT + threadIdx.x;
+      kv[u] = i < hi ? keys[i] : kIneligible;
+      any |= kv[u] == T;
+    }
+    if (!__syncthreads_or(any)) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long i = c0 + u * NT + threadIdx.x;
+        if (i < hi) mask[i] = kv[u] < T;
+      }
+      continue;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = c0 + u * NT + threadIdx.x;
+      const unsigned is_tie = kv[u] == T ? 1u : 0u;
+      unsigned tot;
+      const unsigned ex = block_exclusive_scan(is_tie, warp_sums, &tot);
+      if (i < hi) mask[i] = (kv[u] < T) || (is_tie && run + ex < need);
+      run += tot;
+    }
   }
 }
 
