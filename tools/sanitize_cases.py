@@ -28,5 +28,23 @@ st2._grad_sum.copy_(torch.from_numpy(np.random.default_rng(4).exponential(3e-4, 
 st2._accum_count = 1
 st2.set_edge_score(np.random.default_rng(5).random(n))
 print(int(sharded.select_candidates_sharded(st2, cfg, 2000, n, n).sum()))
+# fused 2-D split through densify_step, a fused split that must not write (budget), scene IO
+m = 500
+sc2 = igs.Scene2(np.random.default_rng(6).normal(size=(m, 2)), np.zeros((m, 2)), np.zeros(m),
+                 np.zeros(m), np.ones((m, 3)), capacity=m + 100)
+st3 = igs.DensifyStats(m)
+igs.accumulate_grads(st3, np.random.default_rng(7).exponential(3e-4, m))
+st3.set_edge_score(np.random.default_rng(8).random(m))
+print(igs.densify_step(sc2, st3, igs.DensifyConfig(budget=m + 100), 2000))
+small = igs.Scene3(pos[:64], ls[:64], q[:64], o[:64], sh[:64], capacity=70)
+try:
+    igs.las_split_batch(small, np.ones(64, bool))
+except igs.BudgetError:
+    pass
+import tempfile
+with tempfile.TemporaryDirectory() as d:
+    igs.write_scene(scene, os.path.join(d, "s.igsp"))
+    back = igs.read_scene(os.path.join(d, "s.igsp"), capacity=scene.count + 10)
+    print(back.count)
 torch.cuda.synchronize()
 print("sanitize cases ok")
