@@ -314,6 +314,7 @@ def run_ours(args, world, rank, local):
         line["e2e"] = e2e_edge(args, world, dev)
     if not args.no_uhd:
         line["edge_uhd"] = bench_uhd(args, world, dev, peak)
+        line["edge_f32_input"] = bench_f32_input(args, world, dev, peak)
     if not args.no_las:
         line["las"] = bench_las(args, world, dev, peak, peak_src)
         line["densify_sharded"] = bench_densify_sharded(args, world, rank, dev)
@@ -359,6 +360,55 @@ def e2e_edge(args, world, dev):
             "bound": "PCIe host->device copy of the float64 views (the kernel takes ~4% of the step)",
             "api": "importance_batch(pinned host views, out=pinned host maps), 8-view chunks "
                    "with H2D / kernel / D2H overlapped on three streams"}
+
+
+def bench_f32_input(args, world, dev, peak):
+    """SURVEY.md 8(d)'s float32-input variant: the same 200 views stored as float32 (12 B/px in,
+    float64 maps out: 20 B/px). The reference converts to float64 first (edge_pipeline.py:133),
+    so the maps are identical to the float64 run on the converted values. Device-resident, plus
+    the end-to-end form with pinned host buffers (8 B/px less over PCIe)."""
+    import torch
+
+    import paper_2603_08661_b200 as igs
+    from paper_2603_08661_b200.synth import synth_views_torch
+    views = synth_views_torch(VIEWS, H, W, seed=1000, device=dev).float()
+    out = torch.empty((VIEWS, H, W), dtype=torch.float64, device=dev)
+    for _ in range(2):
+        igs.importance_batch(views, out=out)
+    steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        igs.importance_batch(views, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    achieved = VIEWS * PX * 20 / (ms * 1e-3) / 1e9
+    host_in = views.cpu().pin_memory()
+    del views
+    host_out = torch.empty((VIEWS, H, W), dtype=torch.float64).pin_memory()
+    for _ in range(1):
+        igs.importance_batch(host_in, out=host_out)
+    torch.cuda.synchronize()
+    esteps = max(2, min(args.steps, 4))
+    t0 = time.perf_counter()
+    for _ in range(esteps):
+        igs.importance_batch(host_in, out=host_out)
+    torch.cuda.synchronize()
+    sec = max_over_ranks((time.perf_counter() - t0) / esteps, world)
+    del out
+    torch.cuda.empty_cache()
+    return {"metric": "edge-map MPix/s", "value": round(world * VIEWS * PX / (ms * 1e-3) / 1e6, 3),
+            "unit": "MPix/s", "ms_per_step": round(ms, 4), "steps": steps, "dtype_in": "f32",
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "algorithmic_bytes_per_px": 20},
+            "e2e": {"value": round(world * VIEWS * PX / sec / 1e6, 3), "unit": "MPix/s",
+                    "h2d_bytes_per_step": VIEWS * PX * 12, "d2h_bytes_per_step": VIEWS * PX * 8,
+                    "ms_per_step": round(sec * 1e3, 3)},
+            "config": {"workload": "the headline's 200 x 1237x822 views as float32 input"}}
 
 
 def bench_las(args, world, dev, peak, peak_src):
