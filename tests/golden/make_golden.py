@@ -85,6 +85,12 @@ def edge_cases():
     g = rng.random((45, 61))
     for s in (0.3, 0.5, 0.7, 2.2, 3.0):
         cases[f"sigma{s}"] = (g, s)
+    # non-finite pixels (their own generator, so the cases above keep their draws)
+    nf = np.floor(np.random.default_rng(77).random((40, 52, 3)) * 255) / 255
+    nf[10, 10, 0] = np.nan
+    nf[25, 30, 2] = np.inf
+    nf[33, 5, 1] = -np.inf
+    cases["nonfinite"] = (nf, 1.0)
     out = {}
     for name, (img, sigma) in cases.items():
         gray = img if img.ndim == 2 else to_grayscale(img)

@@ -44,7 +44,8 @@ def test_golden_stages(case):
     # orientation lives on a circle of circumference pi (pkg/tests/test_edge_pipeline.py:155-158):
     # CUDA's atan2 can land one ulp below pi where glibc rounds to pi (-> 0 after mod pi)
     d = np.abs(f.orientation - c["orientation"])
-    assert (np.minimum(d, np.pi - d) <= 4e-15).all()
+    both_nan = np.isnan(f.orientation) & np.isnan(c["orientation"])  # non-finite pixels
+    assert ((np.minimum(d, np.pi - d) <= 4e-15) | both_nan).all()
     # NMS stage on the reference's own field: bit-exact
     assert_array_equal(b.nms_thin(b.GradientField(c["magnitude"], c["orientation"])),
                        c["thinned"])
@@ -248,3 +249,34 @@ def test_uhd_view_bit_exact():
     got = b.importance_batch(torch.from_numpy(img[None]).cuda()).cpu().numpy()[0]
     want = OE.importance_pipeline(img)
     assert np.flatnonzero(got != want).size == 0
+
+
+@pytest.mark.parametrize("h,w", [(129, 125), (128, 248), (257, 249), (16, 1000), (17, 3),
+                                 (300, 124), (4, 4), (130, 127)])
+def test_band_boundary_shapes(h, w):
+    """Heights and widths at the band tiling's edges (124-column bands, 128-row bands, 16-row
+    sub-steps): every view bit-exact with the oracle, with and without the median stage."""
+    b = B()
+    rng = np.random.default_rng(h * 1000 + w)
+    imgs = np.floor(rng.random((3, h, w, 3)) * 255) / 255
+    got = b.importance_batch(imgs)
+    raw = b.importance_batch(imgs, median=False)
+    for v in range(3):
+        assert_array_equal(got[v], OE.importance_pipeline(imgs[v]), err_msg=f"{h}x{w} v{v}")
+        assert_array_equal(raw[v], OE.importance_pipeline(imgs[v], median=False))
+
+
+def test_non_finite_pixels_match_reference():
+    """NaN / inf pixels propagate through gray, blur and Sobel as in numpy / scipy; the
+    thinned map, the median of the positives and the normalised map still match."""
+    b = B()
+    rng = np.random.default_rng(5)
+    img = np.floor(rng.random((70, 90, 3)) * 255) / 255
+    img[10, 10, 0] = np.nan
+    img[40, 50, 2] = np.inf
+    img[60, 5, 1] = -np.inf
+    want = OE.importance_pipeline(img)
+    got = b.importance_pipeline(img)
+    assert_array_equal(got, want)
+    want_raw = OE.importance_pipeline(img, median=False)
+    assert_array_equal(b.importance_pipeline(img, median=False), want_raw)
