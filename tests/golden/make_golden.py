@@ -200,6 +200,28 @@ def las_cases():
     out["consts/mask"] = mask
     out["consts/capacity"] = np.int64(700)
     out["consts/constants"] = np.array([0.3, 1.0, 0.9])
+    # non-finite log-scales / positions on masked parents (np.argmax takes the first NaN; exp
+    # of +-inf), from their own generator so the cases above keep their draws
+    r2 = np.random.default_rng(909)
+    scene = random_scene(r2, 64, 129)
+    ls = scene.log_scales
+    ls[0, 1] = np.nan
+    ls[1, :] = np.nan
+    ls[2, 2] = np.inf
+    ls[3, 0] = -np.inf
+    ls[4, :] = -np.inf
+    scene.positions[5, 0] = np.nan
+    scene.positions[6, 2] = np.inf
+    mask = np.ones(64, dtype=bool)
+    mask[7] = False
+    before = scene.copy()
+    with np.errstate(all="ignore"):
+        las_split_batch(scene, mask, SplitConstants())
+    for col in ("positions", "log_scales", "rotations", "opacity_logits", "colors"):
+        out[f"nonfinite/in_{col}"] = getattr(before, col)
+        out[f"nonfinite/out_{col}"] = getattr(scene, col)
+    out["nonfinite/mask"] = mask
+    out["nonfinite/capacity"] = np.int64(129)
     # errors the reference raises (recorded as flags)
     s = random_scene(rng, 4, 5)
     try:

@@ -27,9 +27,14 @@ def assert_las_close(got, want, label=""):
         assert_array_equal(got[col], want[col], err_msg=f"{label} {col}")
     gp, wp = got["positions"].astype(np.float64), want["positions"].astype(np.float64)
     assert gp.shape == wp.shape, label
-    scale = np.abs(wp) + np.exp(want["log_scales"].astype(np.float64)).max(axis=1,
-                                                                           keepdims=True) * 2
-    assert (np.abs(gp - wp) <= 1e-5 * scale).all(), f"{label} positions"
+    with np.errstate(all="ignore"):
+        scale = np.abs(wp) + np.exp(want["log_scales"].astype(np.float64)).max(axis=1,
+                                                                               keepdims=True) * 2
+        close = np.abs(gp - wp) <= 1e-5 * scale
+    # non-finite results (NaN / inf log-scales or positions) must match exactly
+    nonfin = ~np.isfinite(wp)
+    close[nonfin] = (gp[nonfin] == wp[nonfin]) | (np.isnan(gp[nonfin]) & np.isnan(wp[nonfin]))
+    assert close.all(), f"{label} positions"
     go, wo = got["opacity_logits"].astype(np.float64), want["opacity_logits"].astype(np.float64)
     assert (np.abs(go - wo) <= 1e-5 * np.maximum(1.0, np.abs(wo))).all(), f"{label} opacity"
 
