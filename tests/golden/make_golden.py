@@ -260,6 +260,34 @@ def select_cases():
                     out[f"{key}/policy"] = np.array(policy)
                     out[f"{key}/mask"] = mask
                     i += 1
+    # non-finite statistics: NaN / inf edge scores and gradient sums in every policy (their own
+    # generator, so the cases above keep their draws)
+    r2 = np.random.default_rng(406)
+    for j, (step, policy) in enumerate((s_, p_) for s_ in (500, 2000)
+                                       for p_ in ("product", "edge", "grad")):
+        n = 300
+        grads = r2.exponential(2e-4, n)
+        grads[r2.random(n) < 0.05] = np.nan
+        grads[r2.random(n) < 0.03] = np.inf
+        edges = np.round(r2.random(n), 2)
+        edges[r2.random(n) < 0.05] = np.nan
+        edges[r2.random(n) < 0.03] = np.inf
+        edges[r2.random(n) < 0.03] = -np.inf
+        stats = DensifyStats(n)
+        with np.errstate(all="ignore"):
+            accumulate_grads(stats, grads)
+        stats.edge_score[:] = edges
+        cfg = DensifyConfig(budget=10 * n, growth_cap=0.3, policy=policy)
+        headroom = n
+        with np.errstate(all="ignore"):
+            mask = select_candidates(stats, cfg, step, headroom)
+        key = f"s_nf{j}"
+        out[f"{key}/grad_sum"] = stats._grad_sum.copy()
+        out[f"{key}/accum"] = np.int64(stats._accum_count)
+        out[f"{key}/edge"] = stats.edge_score.copy()
+        out[f"{key}/params"] = np.array([step, 0.3, headroom, cfg.grad_threshold])
+        out[f"{key}/policy"] = np.array(policy)
+        out[f"{key}/mask"] = mask
     # densify_step end to end (warm-up + late), event tuple recorded
     rng = np.random.default_rng(405)
     for j, step in enumerate((500, 1000, 1500, 2000)):

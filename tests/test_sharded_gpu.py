@@ -129,3 +129,21 @@ def test_sharded_densify_step_matches_single_device(world, backend):
         assert evt == (ev.step, ev.eligible, ev.split, ev.count_after), rank
         for col in ("positions", "log_scales", "rotations", "opacity_logits", "sh"):
             np.testing.assert_array_equal(full[col], want[col], err_msg=f"{col} rank {rank}")
+
+
+def test_world1_sharded_select_reference_golden():
+    """The sharded radix select against the reference's own masks (tests/golden/select.npz),
+    including the non-finite statistics cases (NaN / inf scores and gradient sums)."""
+    import paper_2603_08661_b200 as b
+    from conftest import load_golden
+    from paper_2603_08661_b200 import sharded
+    for name, c in load_golden("select").items():
+        if not name.startswith("s"):
+            continue
+        step, cap, headroom, thr = c["params"]
+        n = len(c["grad_sum"])
+        cfg = b.DensifyConfig(budget=10 * n, growth_cap=float(cap), policy=str(c["policy"]),
+                              grad_threshold=float(thr))
+        st = _stats(b, c["grad_sum"], int(c["accum"]), c["edge"])
+        got = sharded.select_candidates_sharded(st, cfg, int(step), int(headroom), n)
+        np.testing.assert_array_equal(got.cpu().numpy(), c["mask"], err_msg=name)
