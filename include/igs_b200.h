@@ -1,7 +1,7 @@
 /*
  * igs_b200.h -- C ABI of the B200 (sm_100a) densification hot path of ImprovedGS+.
  *
- * One shared library, libigs_b200.so, built from paper_2603_08661_b200/csrc/*.cu.
+ * One shared library, libigs_b200.so, built from every .cu file in paper_2603_08661_b200/csrc/.
  * Every entry point takes plain device pointers, sizes and a cudaStream_t
  * (passed as void*), returns an igs_status (0 == IGS_OK) and never allocates:
  * the caller owns every buffer, including the workspace, whose size the
