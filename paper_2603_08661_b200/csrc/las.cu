@@ -15,8 +15,12 @@
 //                       count + rank; rotations are cloned with one 16-byte
 //                       access and the SH rows with warp-cooperative 16-byte
 //                       copies of the tile's compacted parent list.
-// The host reads {n_split, flags} between prepare and apply (one sync), raising
-// BudgetError / ValueError before any column is written, as the reference does.
+//   las2d_apply_kernel  the same for 2-D scenes (las_split.py:182-197).
+// Two ways to drive them: igs_las_prepare, a host read of {n_split, flags}, the host
+// checks, then igs_las_apply (the sharded path, whose checks are global); or the fused
+// igs_las_split / igs_las2d_split, where the apply pass reads the summary itself and writes
+// nothing when the host is about to raise, so the only host read comes after the split.
+// Either way BudgetError / ValueError leave every column untouched, as in the reference.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
