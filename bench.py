@@ -318,6 +318,7 @@ def run_ours(args, world, rank, local):
     if not args.no_las:
         line["las"] = bench_las(args, world, dev, peak, peak_src)
         line["densify_sharded"] = bench_densify_sharded(args, world, rank, dev)
+        line["aux"] = bench_aux(args, world, dev, peak)
         if rank == 0:
             line["scene_io"] = bench_scene_io(args, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -409,6 +410,61 @@ def bench_f32_input(args, world, dev, peak):
                     "h2d_bytes_per_step": VIEWS * PX * 12, "d2h_bytes_per_step": VIEWS * PX * 8,
                     "ms_per_step": round(sec * 1e3, 3)},
             "config": {"workload": "the headline's 200 x 1237x822 views as float32 input"}}
+
+
+def bench_aux(args, world, dev, peak):
+    """SURVEY.md 8(f) rows 1-2 at the configs[3] cloud size (6M primitives), kernels timed
+    back to back through the C ABI between CUDA events:
+    sample_scores   bilinear samples of 8 resident 1237x822 maps, one view index per point:
+                    16 B position + 4 B view + 4 x 8 B taps + 8 B score = 60 B per point
+    accumulate_position_grads   grad_sum += hypot(g) in float64: 16 B + 8 B + 8 B = 32 B"""
+    import torch
+
+    from paper_2603_08661_b200 import _lib
+    L = _lib.lib()
+    n, nm = DENSIFY_N, 8
+    g = torch.Generator(device=dev).manual_seed(3)
+    maps = torch.rand((nm, H, W), dtype=torch.float64, device=dev, generator=g)
+    pos = torch.stack([torch.rand(n, dtype=torch.float64, device=dev, generator=g) * (W - 1),
+                       torch.rand(n, dtype=torch.float64, device=dev, generator=g) * (H - 1)], 1)
+    view = torch.randint(0, nm, (n,), dtype=torch.int32, device=dev, generator=g)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    grads = torch.randn((n, 2), dtype=torch.float64, device=dev, generator=g) * 1e-4
+    gsum = torch.zeros(n, dtype=torch.float64, device=dev)
+    sh = _lib.stream_handle(dev)
+
+    def timed(fn, k=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(k):
+            fn()
+        c.record()
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(c) / k, world)
+
+    ms_s = timed(lambda: L.igs_sample_scores(maps.data_ptr(), nm, H, W, pos.data_ptr(),
+                                             view.data_ptr(), n, out.data_ptr(),
+                                             flags.data_ptr(), sh))
+    ms_g = timed(lambda: L.igs_accumulate_grad_norms(gsum.data_ptr(), grads.data_ptr(),
+                                                     _lib.IGS_F64, n, sh))
+    del maps, pos, view, out, grads, gsum
+    torch.cuda.empty_cache()
+
+    def line(ms, bpu, what):
+        ach = n * bpu / (ms * 1e-3) / 1e9
+        return {"metric": f"{what} per s", "value": round(world * n / (ms * 1e-3), 1),
+                "kernel_ms": round(ms, 4),
+                "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                             "unit": "GB/s", "frac": round(ach / peak, 4),
+                             "algorithmic_bytes_per_unit": bpu}}
+    return {"sample_scores": line(ms_s, 60, "points"),
+            "accumulate_position_grads": line(ms_g, 32, "primitives"),
+            "config": {"workload": "6M points / primitives (configs[3] size); 8 resident maps",
+                       "timing": "10 back-to-back launches between CUDA events"}}
 
 
 def bench_las(args, world, dev, peak, peak_src):

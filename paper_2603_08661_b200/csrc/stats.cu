@@ -24,15 +24,46 @@ __device__ __forceinline__ float hypotf_glibc(float x, float y) {
   return (float)sqrt(dx * dx + dy * dy);
 }
 
+constexpr int U = 4;  // primitives per thread, every load issued before the arithmetic
+
 template <typename T>
+struct Pair;
+template <>
+struct Pair<double> { using V = double2; };
+template <>
+struct Pair<float> { using V = float2; };
+
+// PAIR: g is aligned for one (gx, gy) vector load per primitive.
+template <typename T, bool PAIR>
 __global__ void __launch_bounds__(NT) accumulate_kernel(double* __restrict__ grad_sum,
                                                         const T* __restrict__ g, long long n) {
-  const long long i = (long long)blockIdx.x * NT + threadIdx.x;
-  if (i >= n) return;
-  double h;
-  if (sizeof(T) == 8) h = hypot_glibc((double)g[2 * i], (double)g[2 * i + 1]);
-  else h = (double)hypotf_glibc((float)g[2 * i], (float)g[2 * i + 1]);
-  grad_sum[i] = grad_sum[i] + h;
+  const long long base = (long long)blockIdx.x * NT * U + threadIdx.x;
+  T gx[U], gy[U];
+  double sum[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const long long i = base + (long long)u * NT;
+    if (i < n) {
+      if (PAIR) {
+        const typename Pair<T>::V v = __ldcs(reinterpret_cast<const typename Pair<T>::V*>(g) + i);
+        gx[u] = v.x;
+        gy[u] = v.y;
+      } else {
+        gx[u] = g[2 * i];
+        gy[u] = g[2 * i + 1];
+      }
+      sum[u] = grad_sum[i];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const long long i = base + (long long)u * NT;
+    if (i >= n) break;
+    double h;
+    if (sizeof(T) == 8) h = hypot_glibc((double)gx[u], (double)gy[u]);
+    else h = (double)hypotf_glibc((float)gx[u], (float)gy[u]);
+    grad_sum[i] = sum[u] + h;
+  }
 }
 
 }  // namespace stats
@@ -47,12 +78,20 @@ int igs_accumulate_grad_norms(double* grad_sum, const void* grads, int dtype, in
   if (n < 0 || (dtype != IGS_F32 && dtype != IGS_F64)) return IGS_ERR_ARGUMENT;
   if (n == 0) return IGS_OK;
   if (!grad_sum || !grads) return IGS_ERR_ARGUMENT;
-  const unsigned blocks = (unsigned)((n + stats::NT - 1) / stats::NT);
+  const unsigned blocks = (unsigned)((n + stats::NT * stats::U - 1) / (stats::NT * stats::U));
   cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == IGS_F64)
-    stats::accumulate_kernel<double><<<blocks, stats::NT, 0, st>>>(grad_sum, (const double*)grads, n);
-  else
-    stats::accumulate_kernel<float><<<blocks, stats::NT, 0, st>>>(grad_sum, (const float*)grads, n);
+  const uintptr_t a = (uintptr_t)grads;
+  if (dtype == IGS_F64) {
+    if (a % 16 == 0)
+      stats::accumulate_kernel<double, true><<<blocks, stats::NT, 0, st>>>(grad_sum, (const double*)grads, n);
+    else
+      stats::accumulate_kernel<double, false><<<blocks, stats::NT, 0, st>>>(grad_sum, (const double*)grads, n);
+  } else {
+    if (a % 8 == 0)
+      stats::accumulate_kernel<float, true><<<blocks, stats::NT, 0, st>>>(grad_sum, (const float*)grads, n);
+    else
+      stats::accumulate_kernel<float, false><<<blocks, stats::NT, 0, st>>>(grad_sum, (const float*)grads, n);
+  }
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }
