@@ -356,12 +356,27 @@ __global__ void __launch_bounds__(NT) las2d_apply_kernel(
   }
   __syncthreads();
   const unsigned long long slot0 = (unsigned long long)count + tile_off[blockIdx.x];
+  // every load of the thread's parents first, then the arithmetic (as the 3-D pass)
+  float lv[PER][2], pv[PER][2], ov[PER], tv[PER], cv[PER][3];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    if (!m[j]) continue;
+    const long long i = base + j * NT + threadIdx.x;
+    lv[j][0] = ls[2 * i];
+    lv[j][1] = ls[2 * i + 1];
+    pv[j][0] = pos[2 * i];
+    pv[j][1] = pos[2 * i + 1];
+    ov[j] = opac[i];
+    tv[j] = theta[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cv[j][k] = col[3 * i + k];
+  }
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     if (!m[j]) continue;
     const long long i = base + j * NT + threadIdx.x;
     const long long dst = (long long)(slot0 + warp_pre[j * (NT / 32) + warp] + wrank[j]);
-    const float l0 = ls[2 * i], l1 = ls[2 * i + 1];
+    const float l0 = lv[j][0], l1 = lv[j][1];
     int l = 0;  // np.argmax: first maximum (a NaN counts as the maximum)
     float best = l0;
     if (!(best != best) && (l1 > best || l1 != l1)) {
@@ -373,12 +388,12 @@ __global__ void __launch_bounds__(NT) las2d_apply_kernel(
     const float cll = best + c.log_alpha;
     if (l == 0) cl0 = cll;
     else cl1 = cll;
-    const float raw = raw_opacity(opac[i], c.beta);
+    const float raw = raw_opacity(ov[j], c.beta);
     const float co = logf(raw / (1.0f - raw));
-    const float th = theta[i];
+    const float th = tv[j];
     const float ct = cosf(th), st = sinf(th);
     const float d0 = (l == 0 ? ct : -st) * offset, d1 = (l == 0 ? st : ct) * offset;
-    const float p0 = pos[2 * i], p1 = pos[2 * i + 1];
+    const float p0 = pv[j][0], p1 = pv[j][1];
     pos[2 * i] = p0 + d0;
     pos[2 * i + 1] = p1 + d1;
     ls[2 * i] = cl0;
@@ -390,9 +405,9 @@ __global__ void __launch_bounds__(NT) las2d_apply_kernel(
     ls[2 * dst + 1] = cl1;
     theta[dst] = th;
     opac[dst] = co;
-    col[3 * dst] = col[3 * i];
-    col[3 * dst + 1] = col[3 * i + 1];
-    col[3 * dst + 2] = col[3 * i + 2];
+    col[3 * dst] = cv[j][0];
+    col[3 * dst + 1] = cv[j][1];
+    col[3 * dst + 2] = cv[j][2];
   }
 }
 

@@ -21,22 +21,33 @@ namespace scene_io {
 
 constexpr int NT = 256;
 
+constexpr int U = 4;  // quaternions per thread, loads first
+
 __global__ void __launch_bounds__(NT) normalize_quats_kernel(float4* __restrict__ q, long long n,
                                                               int* flags) {
-  const long long i = (long long)blockIdx.x * NT + threadIdx.x;
-  if (i >= n) return;
-  const float4 v = q[i];
-  const double x = v.x, y = v.y, z = v.z, w = v.w;
-  double s = x * x;
-  s = s + y * y;
-  s = s + z * z;
-  s = s + w * w;
-  const double norm = sqrt(s);
-  if (!(norm > 0.0) || !isfinite(norm)) {
-    atomicOr(flags, 1);
-    return;
+  const long long base = (long long)blockIdx.x * NT * U + threadIdx.x;
+  float4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const long long i = base + (long long)u * NT;
+    if (i < n) v[u] = q[i];
   }
-  q[i] = make_float4((float)(x / norm), (float)(y / norm), (float)(z / norm), (float)(w / norm));
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const long long i = base + (long long)u * NT;
+    if (i >= n) break;
+    const double x = v[u].x, y = v[u].y, z = v[u].z, w = v[u].w;
+    double s = x * x;
+    s = s + y * y;
+    s = s + z * z;
+    s = s + w * w;
+    const double norm = sqrt(s);
+    if (!(norm > 0.0) || !isfinite(norm)) {
+      atomicOr(flags, 1);
+      continue;
+    }
+    q[i] = make_float4((float)(x / norm), (float)(y / norm), (float)(z / norm), (float)(w / norm));
+  }
 }
 
 }  // namespace scene_io
@@ -52,7 +63,7 @@ int igs_normalize_quaternions(float* quats, int64_t n, int32_t* flags, void* str
   cudaStream_t s = (cudaStream_t)stream;
   IGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int32_t), s));
   if (n == 0) return IGS_OK;
-  const long long blocks = (n + scene_io::NT - 1) / scene_io::NT;
+  const long long blocks = (n + scene_io::NT * scene_io::U - 1) / (scene_io::NT * scene_io::U);
   scene_io::normalize_quats_kernel<<<(unsigned)blocks, scene_io::NT, 0, s>>>(
       reinterpret_cast<float4*>(quats), n, flags);
   IGS_LAUNCH_CHECK();
