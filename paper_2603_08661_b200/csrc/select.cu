@@ -32,6 +32,7 @@ namespace sel {
 constexpr int NT = 512;
 constexpr int NBK = 2048;
 constexpr int PASSES = 6;
+constexpr int U = 4;                     // elements per thread per streaming step
 constexpr unsigned long long kIneligible = ~0ull;
 constexpr int MAX_GRID = 4096;
 
@@ -120,18 +121,31 @@ __global__ void __launch_bounds__(NT) select_kernel(Params P) {
   for (int i = threadIdx.x; i < NBK; i += NT) s.h[i] = 0;
   __syncthreads();
   unsigned elig = 0;
-  for (long long i = lo + threadIdx.x; i < hi; i += NT) {
-    double g = P.accum ? P.grad_sum[i] / (double)P.accum : inv_none;
-    bool e = P.warmup || g > P.thr;
-    double sc;
-    if (P.warmup || P.policy == IGS_POLICY_EDGE) sc = P.edge[i];
-    else if (P.policy == IGS_POLICY_GRAD) sc = g;
-    else sc = P.edge[i] * g;
-    unsigned long long k = e ? score_key(sc) : kIneligible;
-    P.keys[i] = k;
-    if (e) {
-      ++elig;
-      atomicAdd(&s.h[k >> 53], 1u);
+  const bool need_edge = P.warmup || P.policy != IGS_POLICY_GRAD;
+  for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {  // U per thread, loads first
+    double gs[U], ed[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * NT;
+      gs[u] = i < hi ? __ldcs(P.grad_sum + i) : 0.0;
+      ed[u] = (i < hi && need_edge) ? __ldcs(P.edge + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = i0 + u * NT;
+      if (i >= hi) break;
+      double g = P.accum ? gs[u] / (double)P.accum : inv_none;
+      bool e = P.warmup || g > P.thr;
+      double sc;
+      if (P.warmup || P.policy == IGS_POLICY_EDGE) sc = ed[u];
+      else if (P.policy == IGS_POLICY_GRAD) sc = g;
+      else sc = ed[u] * g;
+      unsigned long long k = e ? score_key(sc) : kIneligible;
+      P.keys[i] = k;
+      if (e) {
+        ++elig;
+        atomicAdd(&s.h[k >> 53], 1u);
+      }
     }
   }
   elig = __reduce_add_sync(0xffffffffu, elig);
@@ -163,9 +177,13 @@ __global__ void __launch_bounds__(NT) select_kernel(Params P) {
     __syncthreads();
     const int sh = pass_shift(p);
     const unsigned dm = pass_mask(p);
-    for (long long i = lo + threadIdx.x; i < hi; i += NT) {
-      unsigned long long k = __ldcg(&P.keys[i]);
-      if (k != kIneligible && (k & pmask) == prefix) atomicAdd(&s.h[(k >> sh) & dm], 1u);
+    for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
+      unsigned long long kv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) kv[u] = i0 + u * NT < hi ? __ldcg(&P.keys[i0 + u * NT]) : kIneligible;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (kv[u] != kIneligible && (kv[u] & pmask) == prefix) atomicAdd(&s.h[(kv[u] >> sh) & dm], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < NBK; i += NT)
@@ -186,7 +204,13 @@ __global__ void __launch_bounds__(NT) select_kernel(Params P) {
 
   // per-block tie counts
   unsigned ties = 0;
-  for (long long i = lo + threadIdx.x; i < hi; i += NT) ties += (__ldcg(&P.keys[i]) == T);
+  for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
+    unsigned long long kv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) kv[u] = i0 + u * NT < hi ? __ldcg(&P.keys[i0 + u * NT]) : ~T;
+#pragma unroll
+    for (int u = 0; u < U; ++u) ties += (kv[u] == T);
+  }
   ties = __reduce_add_sync(0xffffffffu, ties);
   if (threadIdx.x == 0) s.u32[1] = 0;
   __syncthreads();
@@ -203,14 +227,33 @@ __global__ void __launch_bounds__(NT) select_kernel(Params P) {
   if (lane_id() == 0 && before) atomicAdd(&s.u64[1], before);
   __syncthreads();
   unsigned long long run = s.u64[1];
-  for (long long c0 = lo; c0 < hi; c0 += NT) {
-    long long i = c0 + threadIdx.x;
-    unsigned long long k = i < hi ? __ldcg(&P.keys[i]) : kIneligible;
-    unsigned is_tie = (k == T) ? 1u : 0u;
-    unsigned tot;
-    unsigned ex = block_exclusive_scan(is_tie, s.warp_sums, &tot);
-    if (i < hi) P.mask[i] = (k < T) || (is_tie && run + ex < need_ties);
-    run += tot;
+  // U-element steps; the tie scan (in index order) only runs for steps that hold a tie
+  for (long long c0 = lo; c0 < hi; c0 += U * NT) {
+    unsigned long long kv[U];
+    int any = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = c0 + u * NT + threadIdx.x;
+      kv[u] = i < hi ? __ldcg(&P.keys[i]) : kIneligible;
+      any |= kv[u] == T;
+    }
+    if (!__syncthreads_or(any)) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long i = c0 + u * NT + threadIdx.x;
+        if (i < hi) P.mask[i] = kv[u] < T;
+      }
+      continue;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = c0 + u * NT + threadIdx.x;
+      const unsigned is_tie = (kv[u] == T) ? 1u : 0u;
+      unsigned tot;
+      const unsigned ex = block_exclusive_scan(is_tie, s.warp_sums, &tot);
+      if (i < hi) P.mask[i] = (kv[u] < T) || (is_tie && run + ex < need_ties);
+      run += tot;
+    }
   }
 }
 
