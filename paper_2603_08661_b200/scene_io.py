@@ -44,23 +44,23 @@ RECORD_FLOATS = {2: 2 + 2 + 1 + 1 + 3, 3: 3 + 3 + 4 + 1 + 3}
 
 
 class FormatError(ValueError):
-    """Corrupt or unsupported file payload."""
+    """Base of the file-format errors (io_cli.py:40-41); a ValueError, as in the reference."""
 
 
 class SceneFormatError(FormatError):
-    """Scene file violates the binary layout."""
+    """An ``.igsp`` file whose bytes do not follow the layout above (io_cli.py:44-45)."""
 
 
 class BadMagicError(SceneFormatError):
-    pass
+    """The first four bytes are not ``IGSP``."""
 
 
 class UnsupportedVersionError(SceneFormatError):
-    pass
+    """A header version this reader does not know."""
 
 
 class SizeMismatchError(SceneFormatError):
-    pass
+    """File length disagrees with the header's count (or the header itself is cut short)."""
 
 
 def _columns(scene):
@@ -213,15 +213,15 @@ def read_scene(path, capacity=None, device=None):
         head = fh.read(min(size, _HEADER.size + _SH_FIELD.size))
     if head[:4] != SCENE_MAGIC:
         if len(head) < 4 and SCENE_MAGIC.startswith(head):
-            raise SizeMismatchError(f"truncated header: {len(head)} bytes")
-        raise BadMagicError(f"bad magic {head[:4]!r}")
+            raise SizeMismatchError(f"file too short for a header ({len(head)} bytes)")
+        raise BadMagicError(f"not an .igsp file (starts with {head[:4]!r})")
     if len(head) < _HEADER.size:
-        raise SizeMismatchError(f"truncated header: {len(head)} bytes")
+        raise SizeMismatchError(f"file too short for a header ({len(head)} bytes)")
     _, version, dims, count = _HEADER.unpack_from(head)
     if version not in (SCENE_VERSION, SCENE_VERSION_SH):
-        raise UnsupportedVersionError(f"unsupported version {version}")
+        raise UnsupportedVersionError(f".igsp version {version} is not supported")
     if dims not in RECORD_FLOATS:
-        raise SceneFormatError(f"dims must be 2 or 3, got {dims}")
+        raise SceneFormatError(f"scene dimensionality {dims} (expected 2 or 3)")
     hlen, k = _HEADER.size, 1
     if version == SCENE_VERSION_SH:
         if dims != 3 or len(head) < hlen + _SH_FIELD.size:
@@ -233,9 +233,8 @@ def read_scene(path, capacity=None, device=None):
     floats = RECORD_FLOATS[dims] + 3 * (k - 1)
     expected = hlen + count * floats * 4
     if size != expected:
-        raise SizeMismatchError(
-            f"payload size {size - hlen} does not match "
-            f"count {count} (expected {expected - hlen})")
+        raise SizeMismatchError(f"{size - hlen} payload bytes for {count} records of {floats} "
+                                f"floats ({expected - hlen} expected)")
     n = int(count)
     cap = max(n, 1) if capacity is None else int(capacity)
     if cap < n:
@@ -278,7 +277,7 @@ def read_scene(path, capacity=None, device=None):
         _lib.check(L.igs_normalize_quaternions(scene._rot.data_ptr(), n, flags.data_ptr(),
                                                _lib.stream_handle(dev)), "read_scene")
         if int(flags.item()):
-            raise SceneFormatError("degenerate quaternion in payload")
+            raise SceneFormatError("a stored rotation has zero or non-finite norm")
     scene._set_count(n)
     torch.cuda.current_stream(dev).synchronize()
     return scene
