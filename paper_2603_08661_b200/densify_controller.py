@@ -136,7 +136,7 @@ def eligible_count(stats: DensifyStats, cfg: DensifyConfig, step: int) -> int:
 
 @dataclass(frozen=True)
 class DensifyEvent:
-    """Log record of one densify step (densify_controller.py:109-119)."""
+    """What one densify event did: step, eligible count, splits, count after (densify_controller.py:109-119)."""
 
     step: int
     eligible: int

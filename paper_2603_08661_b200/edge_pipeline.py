@@ -60,7 +60,7 @@ def _ret(t: torch.Tensor, to_numpy: bool):
 
 @dataclass
 class GradientField:
-    """Per-pixel gradient magnitude (>= 0) and orientation in [0, pi) (edge_pipeline.py:30-39)."""
+    """Sobel output: magnitude and orientation mod pi, same shape (edge_pipeline.py:30-39)."""
 
     magnitude: object
     orientation: object
@@ -71,7 +71,7 @@ class GradientField:
 
 
 def to_grayscale(image):
-    """Rec.601 luma of an (H, W, 3) image, clamped to [0, 1] (edge_pipeline.py:42-49)."""
+    """Gray image from RGB with the Rec.601 weights, clipped to [0, 1] (edge_pipeline.py:42-49)."""
     img, np_out = _as_cuda(image, (torch.float32, torch.float64))
     if img.ndim != 3 or img.shape[2] != 3 or img.shape[0] < 1 or img.shape[1] < 1:
         raise ValueError("expected a non-empty (H, W, 3) image")
@@ -229,7 +229,7 @@ def importance_batch(images, sigma: float = 1.0, *, out=None, nms: bool = True,
 
 
 def sample_scores(importance, positions, view=None):
-    """Bilinearly sample an importance map at (x, y) pixel positions (edge_pipeline.py:138-164);
+    """Importance at (x, y) pixel positions by bilinear interpolation (edge_pipeline.py:138-164);
     positions outside [0, W-1] x [0, H-1] score 0.  Batched form: ``importance`` (B, H, W) and
     ``view`` (N,) int map indices.  numpy in -> numpy out; CUDA tensors -> CUDA tensor."""
     imp, np_out = _as_cuda(importance)

@@ -23,12 +23,12 @@ from .core import Scene2, Scene3
 
 
 class BudgetError(RuntimeError):
-    """Raised when a split would push a scene past its capacity (las_split.py:26-27)."""
+    """A split that needs more rows than the scene reserved (las_split.py:26-27)."""
 
 
 @dataclass(frozen=True)
 class SplitConstants:
-    """Shrink/opacity factors applied to both children of a split (las_split.py:30-49)."""
+    """The split's scale factors (long axis alpha, other axes gamma_axis) and opacity factor beta, validated (las_split.py:30-49)."""
 
     alpha: float = 0.5
     gamma_axis: float = 0.85
