@@ -102,7 +102,7 @@ def _launch_select(stats: DensifyStats, cfg: DensifyConfig, step: int, take_cap:
     n = len(stats)
     L = _lib.lib()
     mask = torch.empty(n, dtype=torch.uint8, device=stats._device)
-    counts = torch.zeros(2, dtype=torch.int64, device=stats._device)
+    counts = torch.empty(2, dtype=torch.int64, device=stats._device)  # the kernel writes both
     nbytes = _lib.query_size(L.igs_select_workspace_bytes, n)
     ws = _lib.workspace(nbytes, stats._device, "select")
     _lib.check(L.igs_select_candidates(
