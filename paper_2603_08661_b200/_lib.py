@@ -128,7 +128,15 @@ def workspace(nbytes: int, device, tag: str) -> torch.Tensor:
     return buf
 
 
+_sizes = {}
+
+
 def query_size(fn, *args) -> int:
-    out = C.c_size_t(0)
-    check(fn(*args, C.byref(out)), fn.__name__)
-    return int(out.value)
+    """A *_workspace_bytes query (pure host arithmetic), memoised per (entry point, shape)."""
+    key = (fn.__name__, args)
+    v = _sizes.get(key)
+    if v is None:
+        out = C.c_size_t(0)
+        check(fn(*args, C.byref(out)), fn.__name__)
+        v = _sizes[key] = int(out.value)
+    return v

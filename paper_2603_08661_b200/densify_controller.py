@@ -97,12 +97,15 @@ def _take_cap(cfg: DensifyConfig, count: int, headroom: int) -> int:
     return min(headroom, max(cap, 0))
 
 
-def _launch_select(stats: DensifyStats, cfg: DensifyConfig, step: int, take_cap: int):
-    """Async select; returns (mask uint8 tensor, counts int64[2] device tensor)."""
+def _launch_select(stats: DensifyStats, cfg: DensifyConfig, step: int, take_cap: int,
+                   counts=None):
+    """Async select; returns (mask uint8 tensor, counts int64[2] device tensor). ``counts``
+    (optional) is the device int64[2] to write {#eligible, take} into."""
     n = len(stats)
     L = _lib.lib()
     mask = torch.empty(n, dtype=torch.uint8, device=stats._device)
-    counts = torch.empty(2, dtype=torch.int64, device=stats._device)  # the kernel writes both
+    if counts is None:
+        counts = torch.empty(2, dtype=torch.int64, device=stats._device)  # the kernel writes both
     nbytes = _lib.query_size(L.igs_select_workspace_bytes, n)
     ws = _lib.workspace(nbytes, stats._device, "select")
     _lib.check(L.igs_select_candidates(
@@ -164,9 +167,10 @@ def densify_step(scene, stats: DensifyStats, cfg: DensifyConfig, step: int) -> D
     c = cfg.split_constants
     if take_cap > 0:
         # select, then the fused split (pre-pass + device-guarded apply); one host read
-        mask, counts = _launch_select(stats, cfg, step, take_cap)
-        summary = _las.split_async(scene, mask.view(torch.bool), c)
-        eligible, _, n_split, flags = (int(v) for v in torch.cat([counts, summary]).cpu())
+        res = torch.empty(4, dtype=torch.int64, device=stats._device)  # counts | split summary
+        mask, _ = _launch_select(stats, cfg, step, take_cap, counts=res[:2])
+        _las.split_async(scene, mask.view(torch.bool), c, summary=res[2:])
+        eligible, _, n_split, flags = (int(v) for v in res.cpu())
         _las.finish_split(scene, n_split, flags)
     else:
         eligible, n_split = eligible_count(stats, cfg, step), 0

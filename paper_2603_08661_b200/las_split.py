@@ -12,6 +12,7 @@ device->host read of {n_split, flags} -> host checks -> ``igs_las_apply``.
 
 from __future__ import annotations
 
+import functools
 import math
 from dataclasses import dataclass
 
@@ -44,9 +45,14 @@ class SplitConstants:
 
     def device_constants(self):
         """float32 (alpha, log alpha, log gamma, beta) exactly as _split_common casts them."""
-        f = np.float32
-        return (float(f(self.alpha)), float(f(math.log(self.alpha))),
-                float(f(math.log(self.gamma_axis))), float(f(self.beta)))
+        return _device_constants(self.alpha, self.gamma_axis, self.beta)
+
+
+@functools.lru_cache(maxsize=64)
+def _device_constants(alpha, gamma_axis, beta):
+    f = np.float32
+    return (float(f(alpha)), float(f(math.log(alpha))), float(f(math.log(gamma_axis))),
+            float(f(beta)))
 
 
 def _mask_tensor(mask, n, device):
@@ -107,15 +113,17 @@ def check_and_apply(prep: _Prepared, n_split: int, flags: int, c: SplitConstants
     return scene.count
 
 
-def split_async(scene, mask, c: SplitConstants):
+def split_async(scene, mask, c: SplitConstants, summary=None):
     """Launch the fused split (igs_las_split / igs_las2d_split): the pre-pass, then the apply
     pass guarded on the device by the pre-pass summary, with no host round trip between them.
-    Returns the summary (device int64[2] = {n_split, flags}), not yet read."""
+    Returns the summary (device int64[2] = {n_split, flags}; written into ``summary`` when
+    given), not yet read."""
     L = _lib.lib()
     m = _mask_tensor(mask, scene.count, scene.device)
     nbytes = _lib.query_size(L.igs_las_workspace_bytes, scene.count)
     ws = _lib.workspace(nbytes, scene.device, "las")
-    summary = torch.empty(2, dtype=torch.int64, device=scene.device)
+    if summary is None:
+        summary = torch.empty(2, dtype=torch.int64, device=scene.device)
     alpha, log_alpha, log_gamma, beta = c.device_constants()
     if isinstance(scene, Scene3):
         _lib.check(L.igs_las_split(scene._pos.data_ptr(), scene._ls.data_ptr(),
