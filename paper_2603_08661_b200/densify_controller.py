@@ -50,9 +50,9 @@ class DensifyStats:
     def reset(self, count: int | None = None):
         if count is None:
             count = len(self)
-        self._grad_sum = torch.zeros(count, dtype=torch.float64, device=self._device)
+        both = torch.zeros(2, count, dtype=torch.float64, device=self._device)  # one fill
+        self._grad_sum, self.edge_score = both[0], both[1]
         self._accum_count = 0
-        self.edge_score = torch.zeros(count, dtype=torch.float64, device=self._device)
 
     def set_edge_score(self, values):
         v = torch.as_tensor(np.asarray(values) if not isinstance(values, torch.Tensor) else values)
@@ -170,7 +170,7 @@ def densify_step(scene, stats: DensifyStats, cfg: DensifyConfig, step: int) -> D
         res = torch.empty(4, dtype=torch.int64, device=stats._device)  # counts | split summary
         mask, _ = _launch_select(stats, cfg, step, take_cap, counts=res[:2])
         _las.split_async(scene, mask.view(torch.bool), c, summary=res[2:])
-        eligible, _, n_split, flags = (int(v) for v in res.cpu())
+        eligible, _, n_split, flags = res.cpu().tolist()
         _las.finish_split(scene, n_split, flags)
     else:
         eligible, n_split = eligible_count(stats, cfg, step), 0
