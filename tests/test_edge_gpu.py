@@ -280,3 +280,21 @@ def test_non_finite_pixels_match_reference():
     assert_array_equal(got, want)
     want_raw = OE.importance_pipeline(img, median=False)
     assert_array_equal(b.importance_pipeline(img, median=False), want_raw)
+
+
+def test_side_streams_and_concurrent_calls():
+    """Every entry point runs on the caller's current stream with a per-stream workspace:
+    two side streams computing different batches concurrently give the default-stream maps."""
+    b = B()
+    views = torch.from_numpy(_views()[:4]).cuda()
+    want = b.importance_batch(views).clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out1 = torch.empty_like(want[:2])
+    out2 = torch.empty_like(want[2:])
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        b.importance_batch(views[:2], out=out1)
+    with torch.cuda.stream(s2):
+        b.importance_batch(views[2:], out=out2)
+    torch.cuda.synchronize()
+    assert torch.equal(out1, want[:2]) and torch.equal(out2, want[2:])
