@@ -319,6 +319,7 @@ def run_ours(args, world, rank, local):
         line["las"] = bench_las(args, world, dev, peak, peak_src)
         line["densify_sharded"] = bench_densify_sharded(args, world, rank, dev)
         line["aux"] = bench_aux(args, world, dev, peak)
+        line["c1"] = bench_c1(args, world, dev)
         if rank == 0:
             line["scene_io"] = bench_scene_io(args, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -465,6 +466,90 @@ def bench_aux(args, world, dev, peak):
             "accumulate_position_grads": line(ms_g, 32, "primitives"),
             "config": {"workload": "6M points / primitives (configs[3] size); 8 resident maps",
                        "timing": "10 back-to-back launches between CUDA events"}}
+
+
+def bench_c1(args, world, dev):
+    """BASELINE.json configs[0] on the GPU: one 1237x822 view's importance map and LAS on 100k
+    SH3 Gaussians (all masked). Latency-bound at this size, so each is timed both through the
+    public call and as a CUDA-graph replay of the same launches ("use CUDA
+    graphs for C1"); the reference times are one process on the host."""
+    import torch
+
+    import paper_2603_08661_b200 as igs
+    from paper_2603_08661_b200.synth import random_cloud_torch, synth_views_torch
+    view = synth_views_torch(1, H, W, seed=3000, device=dev)
+    out = torch.empty((1, H, W), dtype=torch.float64, device=dev)
+    n = 100_000
+    pos, ls, q, o, sh = random_cloud_torch(n, 16, seed=7, device=dev)
+    scene = igs.Scene3(pos, ls, q, o, sh, capacity=2 * n, device=dev)
+    mask = torch.ones(n, dtype=torch.bool, device=dev)
+    c = igs.SplitConstants()
+
+    def events(fn, k=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(k):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b) / k, world)
+
+    def graphed(fn):
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                fn()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return events(g.replay)
+
+    res = {"config": {"workload": "BASELINE.json configs[0]: 1 x 1237x822 RGB f64 view; LAS on "
+                                  "100k SH3 Gaussians, all masked",
+                      "timing": "20 calls / graph replays between CUDA events"}}
+    edge = lambda: igs.importance_batch(view, out=out)  # noqa: E731
+    res["edge_public_ms"] = round(events(edge), 4)
+    split = lambda: igs.las_split.split_async(scene, mask, c)  # noqa: E731
+    try:
+        res["edge_graph_ms"] = round(graphed(edge), 4)
+        res["las_graph_ms"] = round(graphed(split), 4)   # pre-pass + guarded apply, no read
+    except RuntimeError as e:  # capture unsupported here: keep the public-call numbers
+        res["graph_error"] = str(e)[:160]
+    pristine = {k: getattr(scene, k)[:n].clone() for k in ("_pos", "_ls", "_op")}
+    times = []
+    for it in range(23):
+        for k, v in pristine.items():
+            getattr(scene, k)[:n].copy_(v)
+        scene._set_count(n)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        igs.las_split_batch(scene, mask, c)
+        b.record()
+        torch.cuda.synchronize()
+        if it >= 3:
+            times.append(a.elapsed_time(b))
+    res["las_public_ms"] = round(max_over_ranks(statistics.median(times), world), 4)
+    res["edge_MPix_s"] = round(PX / (min(res.get("edge_graph_ms", 1e9), res["edge_public_ms"])
+                                     * 1e-3) / 1e6, 1)
+    res["las_Gaussians_s"] = round(n / (min(res.get("las_graph_ms", 1e9), res["las_public_ms"])
+                                        * 1e-3), 1)
+    if world == 1 and not args.no_cpu and ref_kind() == "reference":
+        from paper_2603_08661_b200.synth import synth_view
+        fn = ref_edge_fn()
+        v = synth_view(H, W, 3000)
+        fn(v)
+        t0 = time.perf_counter()
+        fn(v)
+        res["cpu_reference_edge_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+        rate, _, _ = cpu_las_rate(n)
+        res["cpu_reference_las_ms"] = round(n / rate * 1e3, 1)
+    return res
 
 
 def bench_las(args, world, dev, peak, peak_src):
