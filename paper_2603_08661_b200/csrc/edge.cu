@@ -110,6 +110,7 @@ struct Params {
   double* medians;          // optional (B,) output of the medians
   // scheduling
   int tw, ncols, band_h, TE, TC, TA;
+  int chunk;                // fused mode: survivor entries per C / A task (<= CHUNK)
   int ahead;                // E may run at most `ahead` views past the A front (< RING)
   double kgray[3];          // Rec.601 weights (edge_pipeline.py:22), in the constant bank
   double ktan, ktol;        // tan(pi/8) and the 1e-12 relative margin of the direction bin
@@ -806,7 +807,7 @@ __device__ __noinline__ void find_median_bins(const Params& p, Smem& s, int v) {
   }
   if (threadIdx.x == 0) {  // C tasks: chunks of the survivor list (fused) or of the input
     const unsigned long long ns = p.mode == MODE_FUSED ? __ldcg(&ctl.nsurv) : 0ull;
-    ctl.tca = p.mode == MODE_FUSED ? (unsigned)((ns + CHUNK - 1) / CHUNK) : (unsigned)p.TC;
+    ctl.tca = p.mode == MODE_FUSED ? (unsigned)((ns + p.chunk - 1) / p.chunk) : (unsigned)p.TC;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -920,7 +921,7 @@ __device__ __noinline__ void run_collect(const Params& p, Smem& s, int v, int c)
   unsigned* h2b = h2a + NB2;
   double* sla = p.slots + (long long)slot * 2 * NB2 * SLOTS;
   double* slb = sla + NB2 * SLOTS;
-  const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, nsrc);
+  const long long lo = (long long)c * p.chunk, hi = min(lo + (long long)p.chunk, nsrc);
   auto bucket = [&](double x, int list) {  // level-2 bucket (returning global atomic)
     const int sb = sub_bin((unsigned long long)__double_as_longlong(x));
     const unsigned k = atomicAdd(&(list ? h2b : h2a)[sb], 1u);
@@ -1147,7 +1148,7 @@ __device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, u
     const double* sval = ring_slot(p, v);
     const unsigned* sidx = surv_idx(p, v);
     const long long n = (long long)__ldcg(&ctl.nsurv);
-    const long long lo = (long long)c * CHUNK, hi = min(lo + (long long)CHUNK, n);
+    const long long lo = (long long)c * p.chunk, hi = min(lo + (long long)p.chunk, n);
     const int npieces = (int)((hi - lo + APIECE - 1) / APIECE);
     double* vbuf = arena(s);
     unsigned* ibuf = reinterpret_cast<unsigned*>(arena(s) + NBUF * APIECE);
@@ -1477,7 +1478,16 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   } else {
     p.TE = (int)((p.npx + CHUNK - 1) / CHUNK);
   }
-  p.TC = median ? (int)((p.npx + CHUNK - 1) / CHUNK) : 0;
+  // fused mode: survivor entries per collect / apply task (16384; small batches use shorter
+  // tasks so the median passes of a few views spread over more CTAs)
+  p.chunk = CHUNK;
+  if (p.mode == MODE_FUSED && p.B <= 8) p.chunk = CHUNK / 4;
+  if (const char* e = getenv("IGS_CHUNK")) {  // tuning override: a multiple of APIECE
+    const int c = atoi(e);
+    if (c >= APIECE && c <= CHUNK && c % APIECE == 0) p.chunk = c;
+  }
+  if (p.mode != MODE_FUSED) p.chunk = CHUNK;
+  p.TC = median ? (int)((p.npx + p.chunk - 1) / p.chunk) : 0;
   p.TA = p.TC;
   const bool fast = p.sym && !p.skip;
   KernelFn fn = nullptr;

@@ -298,3 +298,18 @@ def test_side_streams_and_concurrent_calls():
         b.importance_batch(views[2:], out=out2)
     torch.cuda.synchronize()
     assert torch.equal(out1, want[:2]) and torch.equal(out2, want[2:])
+
+
+def test_large_batch_task_sizes_bit_exact():
+    """A batch above 8 views takes the default task sizes (128-row bands, 16384-entry collect /
+    apply tasks, several per view); smaller batches take shorter ones. Both bit-exact."""
+    from paper_2603_08661_b200.synth import synth_view
+    b = B()
+    views = np.stack([synth_view(822, 1237, 9000 + k) for k in range(10)])
+    got = b.importance_batch(views)
+    small = b.importance_batch(views[:2])
+    for v in (0, 1, 9):
+        want = OE.importance_pipeline(views[v])
+        assert_array_equal(got[v], want, err_msg=f"view {v}")
+        if v < 2:
+            assert_array_equal(small[v], want, err_msg=f"small batch view {v}")
