@@ -282,6 +282,7 @@ def run_ours(args, world, rank, local):
         barrier(world)
     ms = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms, world)
+    check = None if args.no_check else check_sample(views, out)
     value = world * VIEWS * PX / (ms * 1e-3) / 1e6
     algo_bytes = VIEWS * PX * BYTES_PER_PX_F64
     achieved = algo_bytes / (ms * 1e-3) / 1e9
@@ -307,6 +308,7 @@ def run_ours(args, world, rank, local):
                      "note": "the kernel is issue/latency-bound (FP64 blur + integer NMS work); "
                              "fp64 / issue figures from the committed ncu --set full capture"},
         "per_gpu_value": round(value / world, 3),
+        "check": check,
         "clocks": clk.summary(),
         "gpu_launches": args.steps,
     }
@@ -332,6 +334,26 @@ def run_ours(args, world, rank, local):
                                           + " on the host cores"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+CHECK_VIEWS = (0, 16, 99, 199)
+
+
+def check_sample(views, out):
+    """The timed launch's own output for a sample of views (both sides of the 16-slot ring's
+    wraps) against the CPU path the cpu_baseline leg times (the unmodified reference from
+    baseline/_ref, else the oracle restatement) on the same views, outside the timed region:
+    bit-exact or the line says so."""
+    import numpy as np
+    fn = ref_edge_fn()
+    res = {}
+    for v in CHECK_VIEWS:
+        want = fn(views[v].cpu().numpy())
+        res[str(v)] = int(np.count_nonzero(out[v].cpu().numpy() != want))
+    return {"views": list(CHECK_VIEWS), "differing_pixels": res,
+            "bit_exact": all(n == 0 for n in res.values()),
+            "against": ("splitkit.edge_pipeline.importance_pipeline (baseline/_ref)"
+                        if ref_kind() == "reference" else "oracle/edge.py")}
 
 
 def e2e_edge(args, world, dev):
@@ -812,6 +834,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-las", action="store_true")
     ap.add_argument("--no-uhd", action="store_true")
+    ap.add_argument("--no-check", action="store_true",
+                    help="skip the oracle check of a sample of the timed views")
     args = ap.parse_args()
     args.steps_given = args.steps is not None
     if args.steps is None:

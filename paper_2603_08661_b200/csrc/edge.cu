@@ -88,7 +88,8 @@ struct ViewCtl {            // per-view control block, zeroed before launch
   unsigned c_claim, a_claim;// C / A chunks handed out
   unsigned nsurv;           // fused mode: positive survivors appended by the E tasks
   unsigned tca;             // C / A tasks of this view (fused: survivor chunks)
-  unsigned pad[10];
+  unsigned a_done;          // A tasks finished: the view's ring slot is free once a_done == tca
+  unsigned pad[9];
 };
 static_assert(sizeof(ViewCtl) == 128, "one ViewCtl per 128-byte line");
 
@@ -157,7 +158,9 @@ struct __align__(16) Smem {
   int task_kind, task_view, task_idx, flag;
   int ivals[4];
   int scratch[4];
-  unsigned long long mbar[4];  // bulk-copy barriers of the C / A streams (NBUF)
+  unsigned long long mbar[4];  // bulk-copy barriers of the C / A streams (NBUF), initialised once
+  unsigned mbar_seq;           // bulk-copy pieces issued by this CTA so far (barrier phases)
+  int pend_valid, pend_view, pend_idx;  // a claimed band deferred until its ring slot is free
   unsigned long long u64[2];
 };
 
@@ -224,6 +227,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// generic-proxy writes of other CTAs (survivor lists, acquired through the view's control
+// block) -> async-proxy reads (bulk copies from global memory)
+__device__ __forceinline__ void fence_proxy_async_all() {
+  asm volatile("fence.proxy.async;" ::: "memory");
 }
 
 __device__ __forceinline__ double2 ld_cg2(const double* a) {
@@ -849,22 +857,24 @@ __device__ void stream_chunk(Smem& s, const double* src, long long lo, long long
   }
   const long long nfull = n & ~1ll;  // bulk part: a multiple of 16 bytes
   const int npieces = (int)((nfull + PIECE - 1) / PIECE);
+  // barriers initialised once per CTA (kernel prologue); piece j of the CTA's bulk-copy
+  // sequence uses barrier j % NBUF at parity (j / NBUF) & 1
+  __syncthreads();
+  const unsigned seq = s.mbar_seq;
   auto issue = [&](int k) {
     const long long off = (long long)k * PIECE;
     const unsigned len = (unsigned)min((long long)PIECE, nfull - off);
-    bulk_load(arena(s) + (k % NBUF) * PIECE, src + lo + off, len * 8u, &s.mbar[k % NBUF]);
+    bulk_load(arena(s) + (k % NBUF) * PIECE, src + lo + off, len * 8u, &s.mbar[(seq + k) % NBUF]);
   };
-  __syncthreads();
   if (threadIdx.x == 0) {
-    for (int k = 0; k < NBUF; ++k) mbar_init(&s.mbar[k]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    fence_proxy_async();
+    fence_proxy_async();      // earlier generic smem accesses of the arena -> async-proxy writes
+    fence_proxy_async_all();  // survivor lists written by other CTAs -> async-proxy reads
     for (int k = 0; k < NBUF && k < npieces; ++k) issue(k);
   }
   __syncthreads();
   for (int k = 0; k < npieces; ++k) {
     const double* buf = arena(s) + (k % NBUF) * PIECE;
-    mbar_wait(&s.mbar[k % NBUF], (unsigned)((k / NBUF) & 1));
+    mbar_wait(&s.mbar[(seq + k) % NBUF], ((seq + k) / NBUF) & 1u);
     const long long off = (long long)k * PIECE;
     const int len = (int)min((long long)PIECE, nfull - off);
     for (int i = threadIdx.x; i < len; i += NT) visit(lo + off + i, buf[i]);
@@ -874,6 +884,7 @@ __device__ void stream_chunk(Smem& s, const double* src, long long lo, long long
       issue(k + NBUF);
     }
   }
+  if (threadIdx.x == 0) s.mbar_seq = seq + (unsigned)npieces;  // read again after a barrier
   if ((n & 1) && threadIdx.x == 0) visit(hi - 1, __ldcg(src + hi - 1));
   __syncthreads();
 }
@@ -1152,35 +1163,35 @@ __device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, u
     const int npieces = (int)((hi - lo + APIECE - 1) / APIECE);
     double* vbuf = arena(s);
     unsigned* ibuf = reinterpret_cast<unsigned*>(arena(s) + NBUF * APIECE);
+    __syncthreads();
+    const unsigned seq = s.mbar_seq;
     auto issue = [&](int k) {
       const long long off = lo + (long long)k * APIECE;
       const unsigned len = (unsigned)min((long long)APIECE, hi - off);
       const unsigned len4 = (len + 3u) & ~3u;  // 16-byte multiple for the index copy
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                       smem_u32(&s.mbar[k % NBUF])),
+      unsigned long long* bar = &s.mbar[(seq + k) % NBUF];
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                    "r"(len4 * 12u)
                    : "memory");
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
               "r"(smem_u32(vbuf + (k % NBUF) * APIECE)),
-          "l"(sval + off), "r"(len4 * 8u), "r"(smem_u32(&s.mbar[k % NBUF]))
+          "l"(sval + off), "r"(len4 * 8u), "r"(smem_u32(bar))
           : "memory");
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
               "r"(smem_u32(ibuf + (k % NBUF) * APIECE)),
-          "l"(sidx + off), "r"(len4 * 4u), "r"(smem_u32(&s.mbar[k % NBUF]))
+          "l"(sidx + off), "r"(len4 * 4u), "r"(smem_u32(bar))
           : "memory");
     };
-    __syncthreads();
     if (threadIdx.x == 0) {
-      for (int k = 0; k < NBUF; ++k) mbar_init(&s.mbar[k]);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       fence_proxy_async();
+      fence_proxy_async_all();
       for (int k = 0; k < NBUF && k < npieces; ++k) issue(k);
     }
     __syncthreads();
     for (int k = 0; k < npieces; ++k) {
-      mbar_wait(&s.mbar[k % NBUF], (unsigned)((k / NBUF) & 1));
+      mbar_wait(&s.mbar[(seq + k) % NBUF], ((seq + k) / NBUF) & 1u);
       const long long off = lo + (long long)k * APIECE;
       const int len = (int)min((long long)APIECE, hi - off);
       const double* vb = vbuf + (k % NBUF) * APIECE;
@@ -1195,6 +1206,7 @@ __device__ __noinline__ void run_apply(const Params& p, Smem& s, int v, int c, u
         issue(k + NBUF);
       }
     }
+    if (threadIdx.x == 0) s.mbar_seq = seq + (unsigned)npieces;
     return;
   }
   const double* src = (const double*)p.img + (long long)v * p.npx;
@@ -1227,9 +1239,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
+// Ring slot v % RING is free for view v once view v - RING has retired: its median is
+// published and every one of its apply tasks (the last readers of the slot) has finished.
+__device__ __forceinline__ bool ring_free(const Params& p, unsigned v) {
+  if (v < (unsigned)RING) return true;
+  const ViewCtl& old = p.ctl[v - RING];
+  return ld_acquire(&old.select_done) && ld_acquire(&old.a_done) >= __ldcg(&old.tca);
+}
+
+__device__ void claim_task(const Params& p, Smem& s, int& kind, int& view, int& idx) {
   unsigned* sched = p.sched;
   const unsigned B = (unsigned)p.B;
+  // a band claimed earlier whose ring slot was still in use runs as soon as the slot is free
+  if (s.pend_valid && ring_free(p, (unsigned)s.pend_view)) {
+    kind = TASK_E; view = s.pend_view; idx = s.pend_idx;
+    s.pend_valid = 0;
+    return;
+  }
   if (p.median) {
     for (;;) {  // A
       const unsigned v = ld_acquire(&sched[2]);
@@ -1252,16 +1278,32 @@ __device__ void claim_task(const Params& p, int& kind, int& view, int& idx) {
       }
       atomicCAS(&sched[1], v, v + 1);
     }
+    if (s.pend_valid) {  // at most one deferred band per CTA
+      kind = TASK_NONE;
+      return;
+    }
   }
   const unsigned long long total_e = (unsigned long long)p.B * p.TE;
   unsigned long long* e_next = (unsigned long long*)&sched[4];
   unsigned long long t = ld_acquire64(e_next);
-  // throttle (racy by design: concurrent claimers may overshoot by about one view)
+  // throttle: E at most `ahead` views past the A front (racy by design: concurrent claimers
+  // may overshoot; the ring guard below makes an overshoot safe).  A claim is one atomicAdd:
+  // a compare-and-swap claim serialises the grid on the atomic's round trip.
   if (t < total_e && !(p.median && t / p.TE >= ld_acquire(&sched[2]) + (unsigned)p.ahead)) {
-    t = atomicAdd(e_next, 1ull);  // an atomicAdd never retries, unlike a CAS claim
+    t = atomicAdd(e_next, 1ull);
     if (t < total_e) {
       const unsigned v = (unsigned)(t / p.TE);
-      kind = TASK_E; view = (int)v; idx = (int)(t - (unsigned long long)v * p.TE);
+      const int i = (int)(t - (unsigned long long)v * p.TE);
+      if (p.median && !ring_free(p, v)) {
+        // view v - RING still reads ring slot v % RING: defer the band (this CTA keeps
+        // running collect / apply work meanwhile, so older views always make progress)
+        s.pend_view = (int)v;
+        s.pend_idx = i;
+        s.pend_valid = 1;
+        kind = TASK_NONE;
+        return;
+      }
+      kind = TASK_E; view = (int)v; idx = i;
       return;
     }
   }
@@ -1310,7 +1352,7 @@ __device__ void claim_next(const Params& p, Smem& s, unsigned long long pol_in) 
   // called by a whole warp: lane 0 claims, the warp prefetches the first rows of a band
   if ((threadIdx.x & 31) == 0) {
     int nk = 0, nv = 0, ni = 0;
-    claim_task(p, nk, nv, ni);
+    claim_task(p, s, nk, nv, ni);
     s.task_kind = nk;
     s.task_view = nv;
     s.task_idx = ni;
@@ -1325,12 +1367,18 @@ __global__ void __launch_bounds__(NT, IGS_MINB) edge_persistent_kernel(const __g
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   for (int i = threadIdx.x; i < NB / 2; i += NT) s.hist[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 4; ++k) mbar_init(&s.mbar[k]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s.mbar_seq = 0;
+    s.pend_valid = 0;
+  }
   const unsigned long long pol_in = policy_evict_first();
   const unsigned long long pol_mid = policy_evict_last();
   const unsigned long long pol_out = policy_evict_first();
   if (threadIdx.x == 0) {
     int kind = 0, view = 0, idx = 0;
-    claim_task(p, kind, view, idx);
+    claim_task(p, s, kind, view, idx);
     s.task_kind = kind;
     s.task_view = view;
     s.task_idx = idx;
@@ -1374,6 +1422,11 @@ __global__ void __launch_bounds__(NT, IGS_MINB) edge_persistent_kernel(const __g
       if (s.flag) run_select(p, s, v);
     } else if (kind == TASK_A) {
       run_apply(p, s, v, idx, pol_out);
+      __syncthreads();
+      if (threadIdx.x == 0) {  // every read of the ring slot by this task has landed
+        __threadfence();
+        atomicAdd(&p.ctl[v].a_done, 1u);
+      }
     } else if (threadIdx.x == 0) {
       __nanosleep(1000);
     }

@@ -30,13 +30,18 @@ def _dev():
 
 class DensifyStats:
     """Per-primitive selection signals between densify events (densify_controller.py:23-51),
-    float64 on the device."""
+    float64 on the device.
+
+    ``edge_score`` is assignable like the reference's attribute (``stats.edge_score =
+    sample_scores(...)``, splat2d.py:397): numpy arrays and tensors of any float dtype on any
+    device are converted and copied into the device buffer the kernels read, after a length
+    check, so the selection never sees a host pointer, a short buffer or the wrong dtype."""
 
     def __init__(self, count: int, device=None):
         self._device = torch.device(device) if device is not None else _dev()
         self._grad_sum = torch.zeros(count, dtype=torch.float64, device=self._device)
         self._accum_count = 0
-        self.edge_score = torch.zeros(count, dtype=torch.float64, device=self._device)
+        self._edge = torch.zeros(count, dtype=torch.float64, device=self._device)
 
     def __len__(self):
         return self._grad_sum.shape[0]
@@ -47,16 +52,29 @@ class DensifyStats:
             return torch.zeros_like(self._grad_sum)
         return self._grad_sum / self._accum_count
 
+    @property
+    def edge_score(self):
+        return self._edge
+
+    @edge_score.setter
+    def edge_score(self, values):
+        v = values if isinstance(values, torch.Tensor) else torch.as_tensor(np.asarray(values))
+        if v.dtype == torch.bool or v.is_complex():
+            raise TypeError(f"edge scores must be real numbers, got {v.dtype}")
+        if v.ndim != 1 or v.shape[0] != len(self):
+            raise ValueError(f"edge score length {tuple(v.shape)} does not match stats length "
+                             f"({len(self)},)")
+        self._edge.copy_(v.to(self._device, torch.float64))
+
     def reset(self, count: int | None = None):
         if count is None:
             count = len(self)
         both = torch.zeros(2, count, dtype=torch.float64, device=self._device)  # one fill
-        self._grad_sum, self.edge_score = both[0], both[1]
+        self._grad_sum, self._edge = both[0], both[1]
         self._accum_count = 0
 
     def set_edge_score(self, values):
-        v = torch.as_tensor(np.asarray(values) if not isinstance(values, torch.Tensor) else values)
-        self.edge_score.copy_(v.to(self._device, torch.float64).reshape(-1))
+        self.edge_score = values
 
 
 def accumulate_grads(stats: DensifyStats, step_grad_norms) -> DensifyStats:
