@@ -228,20 +228,30 @@ def cpu_las_rate(n=200_000):
         f"{reps} x {n // 1000}k all-masked, SH degree 3, oracle/las.py"
 
 
+def edge_config(world):
+    """The headline line's config, shared by both arms (the driver compares them key by key)."""
+    return {"workload": "200 x 1237x822 RGB f64 views per GPU: gray+blur+Sobel+NMS+"
+                        "median normalisation (BASELINE.json configs[1])",
+            "views_per_gpu": VIEWS, "height": H, "width": W, "io": "f64 in / f64 out",
+            "l2": "inputs 4.9 GB per GPU >> 126 MB L2 (no flush needed)",
+            "parallelism": f"views sharded, {world} GPU(s), no data-path collective"}
+
+
 def run_reference(args, world, rank):
+    """The reference arm: the unmodified splitkit importance_pipeline (baseline/_ref, else the
+    oracle port) on all host cores, with the same --steps / --warmup and config as the GPU arm;
+    each step is a bounded sample of the workload (one 1237x822 view per host process), and
+    the metric is the same per-pixel throughput."""
     if rank != 0:
         return
-    steps = max(1, args.steps if args.steps_given else 5)
-    warmup = max(0, min(args.warmup, 2))
+    steps, warmup = args.steps, args.warmup
     rate, procs, sec = cpu_edge_rate(steps, warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(rate, 3), "unit": "MPix/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "200 x 1237x822 RGB f64 views: gray+blur+Sobel+NMS+median "
-                               "(BASELINE.json configs[1])", "views_per_gpu": VIEWS,
-                   "height": H, "width": W},
+        "config": edge_config(world),
         "cpu_baseline": {"value": round(rate, 3), "unit": "MPix/s", "cores": procs,
                          "kind": ref_kind(),
                          "sample": f"{procs} views per step (1 per process), "
@@ -292,11 +302,7 @@ def run_ours(args, world, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "200 x 1237x822 RGB f64 views per GPU: gray+blur+Sobel+NMS+"
-                               "median normalisation (BASELINE.json configs[1])",
-                   "views_per_gpu": VIEWS, "height": H, "width": W, "io": "f64 in / f64 out",
-                   "l2": "inputs 4.9 GB per GPU >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"views sharded, {world} GPU(s), no data-path collective"},
+        "config": edge_config(world),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": (round(traffic * VIEWS * PX) if traffic else None),
@@ -365,7 +371,7 @@ def e2e_edge(args, world, dev):
     from paper_2603_08661_b200.synth import synth_views_torch
     host_in = synth_views_torch(VIEWS, H, W, seed=2000, device=dev).cpu().pin_memory()
     host_out = torch.empty((VIEWS, H, W), dtype=torch.float64).pin_memory()
-    steps = max(2, min(args.steps, 5))
+    steps = max(3, min(args.steps, 20))
     for _ in range(2):
         igs.importance_batch(host_in, out=host_out)
     barrier(world)
@@ -630,6 +636,21 @@ def bench_las(args, world, dev, peak, peak_src):
     c.record()
     torch.cuda.synchronize()
     ms_kernel = max_over_ranks(a.elapsed_time(c) / K, world)
+    # the public call's device work: igs_las_split (cooperative pre-pass + guarded apply), K
+    # back-to-back launches at the same count (each splits all n parents again)
+    summ = torch.zeros(2, dtype=torch.int64, device=dev)
+    split_args = apply_args[:13] + (prep.ws.data_ptr(), prep.ws.numel(), summ.data_ptr(),
+                                    _lib.stream_handle(dev))
+    restore()
+    for _ in range(2):
+        _lib.check(L.igs_las_split(*split_args), "las bench")
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(K):
+        L.igs_las_split(*split_args)
+    c.record()
+    torch.cuda.synchronize()
+    ms_split = max_over_ranks(a.elapsed_time(c) / K, world)
     restore()
     achieved = n * LAS_BYTES_PER_SPLIT / (ms_kernel * 1e-3) / 1e9
     # full densify_step on the same cloud: select (take = 5% = 50k) + LAS
@@ -662,8 +683,13 @@ def bench_las(args, world, dev, peak, peak_src):
                         "traffic": (round(las_traffic * n) if las_traffic else None),
                         "kernel": "las_apply_kernel", "algorithmic_bytes_per_split": 500,
                         "kernel_ms": round(ms_kernel, 4), "peak_source": peak_src,
+                        "split_device_ms": round(ms_split, 4),
+                        "split_device_frac": round(n * LAS_BYTES_PER_SPLIT / (ms_split * 1e-3)
+                                                   / 1e9 / peak, 4),
                         "timing": "kernel_ms: 10 back-to-back apply launches between CUDA "
-                                  "events; ms_per_step: the public las_split_batch call"},
+                                  "events; split_device_ms: 10 back-to-back igs_las_split "
+                                  "(cooperative pre-pass + guarded apply); ms_per_step: the "
+                                  "public las_split_batch call (host work + one stream sync)"},
            "densify_step": {"ms": round(ds_ms, 4), "n": n, "split": ev.split,
                             "eligible": ev.eligible,
                             "note": "select (radix top-k, take=ceil(0.05 N)) + LAS + one host "

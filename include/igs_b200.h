@@ -52,6 +52,9 @@ enum igs_las_flags {
 const char* igs_strerror(int status);
 const char* igs_last_cuda_error(void);
 int igs_abi_version(void);
+/* cudaStreamSynchronize(stream): the host half of a synchronous call whose kernels write
+ * their result into pinned host memory (e.g. igs_las_split's summary). */
+int igs_stream_synchronize(void* stream);
 
 /* L2 set-aside for persisting (evict_last) lines: the fused edge kernel keeps the in-flight
  * views' thinned maps evict_last.  Device-wide (cudaLimitPersistingL2CacheSize), clamped to
@@ -182,11 +185,13 @@ int igs_las_apply(float* positions, float* log_scales, float* rotations, float* 
                   float beta, int renormalize, void* workspace, size_t workspace_bytes,
                   void* stream);
 
-/* The whole split in one call, no host round trip between the passes: igs_las_prepare, then
- * the apply pass guarded on the device by the summary it wrote.  If count + n_split >
- * capacity or a domain flag (BAD_QUAT / BAD_OPACITY) is set, nothing in the scene is written;
- * the caller reads summary {n_split, flags} afterwards and raises (BudgetError / ValueError)
- * or adds n_split to its count.  Renormalisation follows the summary's RENORM flag. */
+/* The whole split in ONE cooperative launch, no host round trip between the passes: the
+ * pre-pass of every tile, a grid barrier, then the apply pass guarded on the device by the
+ * pre-pass totals.  If count + n_split > capacity or a domain flag (BAD_QUAT / BAD_OPACITY) is
+ * set, nothing in the scene is written; the caller reads summary {n_split, flags} afterwards
+ * and raises (BudgetError / ValueError) or adds n_split to its count.  Renormalisation follows
+ * the RENORM flag.  summary may be device memory or pinned host memory (written directly).
+ * Replaces las_split.py:158-179 (the reference's las_split_batch) in one call. */
 int igs_las_split(float* positions, float* log_scales, float* rotations, float* opacity_logits,
                   float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
                   const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,

@@ -30,6 +30,7 @@ SIGNATURES = {
     "igs_strerror": (C.c_char_p, [_int]),
     "igs_last_cuda_error": (C.c_char_p, []),
     "igs_abi_version": (_int, []),
+    "igs_stream_synchronize": (_int, [_vp]),
     "igs_l2_set_aside": (_int, [_sz, _szp]),
     "igs_edge_workspace_bytes": (_int, [_i64, _i64, _i64, _int, _szp]),
     "igs_edge_importance": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _int, _vp, _vp, _sz,
@@ -86,12 +87,18 @@ def load(path: str = LIB_PATH):
     return _lib
 
 
+_cuda_ok = False
+
+
 def lib():
-    """The library, after checking that a CUDA device is present."""
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2603_08661_b200 needs a CUDA device (sm_100a); "
-                           "there is no CPU fallback")
-    return load()
+    """The library, after checking (once) that a CUDA device is present."""
+    global _cuda_ok
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2603_08661_b200 needs a CUDA device (sm_100a); "
+                               "there is no CPU fallback")
+        _cuda_ok = True
+    return _lib if _lib is not None else load()
 
 
 def check(status: int, what: str):
@@ -106,7 +113,18 @@ def check(status: int, what: str):
     raise RuntimeError(f"{what}: {msg}")
 
 
+try:  # the raw cudaStream_t of the current stream without building a Stream object
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover - older torch
+    _raw_stream = None
+
+
 def stream_handle(device=None) -> int:
+    if _raw_stream is not None:
+        idx = torch.cuda.current_device() if device is None else torch.device(device).index
+        if idx is None:
+            idx = torch.cuda.current_device()
+        return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -120,7 +138,7 @@ _ws: dict = {}
 def workspace(nbytes: int, device, tag: str) -> torch.Tensor:
     """Caller-owned scratch (the library never allocates), cached per (device, stream, tag)."""
     device = torch.device(device)
-    key = (device.index, torch.cuda.current_stream(device).cuda_stream, tag)
+    key = (device.index, stream_handle(device), tag)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)

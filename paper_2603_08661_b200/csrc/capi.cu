@@ -43,6 +43,13 @@ const char* igs_last_cuda_error(void) { return igs::g_cuda_error; }
 
 int igs_abi_version(void) { return 1; }
 
+// Wait for `stream` (the host half of a synchronous call such as las_split_batch, whose
+// kernels write their summary into pinned host memory).
+int igs_stream_synchronize(void* stream) {
+  IGS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return IGS_OK;
+}
+
 // L2 set-aside for persisting (evict_last) lines on the current device; returns the granted
 // size in *granted (nullable).  Device-wide setting (cudaLimitPersistingL2CacheSize).
 int igs_l2_set_aside(size_t bytes, size_t* granted) {

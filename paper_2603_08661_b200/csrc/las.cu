@@ -21,6 +21,7 @@
 // igs_las_split / igs_las2d_split, where the apply pass reads the summary itself and writes
 // nothing when the host is about to raise, so the only host read comes after the split.
 // Either way BudgetError / ValueError leave every column untouched, as in the reference.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -36,8 +37,10 @@ constexpr int TILE = NT * PER;  // Gaussians per block
 constexpr int SUBS = PER * NT / 32;  // (sub-tile, warp) ballot groups per tile
 static_assert(SUBS <= 32, "one warp scans the tile");
 
+constexpr int MAX_CTAS = 2048;  // fused split: per-CTA totals / flags (grid <= 8 x SMs)
+
 struct Layout {
-  size_t tile_cnt, tile_off, total;
+  size_t tile_cnt, tile_off, cta_tot, cta_flag, guard, total;
 };
 
 Layout layout(long long count) {
@@ -45,7 +48,10 @@ Layout layout(long long count) {
   long long tiles = (count + TILE - 1) / TILE;
   L.tile_cnt = 0;
   L.tile_off = align_up(sizeof(unsigned) * (size_t)(tiles + 1), 256);
-  L.total = L.tile_off + align_up(sizeof(unsigned long long) * (size_t)(tiles + 1), 256);
+  L.cta_tot = L.tile_off + align_up(sizeof(unsigned long long) * (size_t)(tiles + 1), 256);
+  L.cta_flag = L.cta_tot + sizeof(unsigned long long) * MAX_CTAS;
+  L.guard = L.cta_flag + sizeof(unsigned) * MAX_CTAS;  // the summary's device copy
+  L.total = L.guard + 2 * sizeof(unsigned long long);
   return L;
 }
 
@@ -65,14 +71,14 @@ __device__ __forceinline__ float raw_opacity(float o, float beta) {
   return s * beta;
 }
 
-__global__ void __launch_bounds__(NT) las_prepare_kernel(const uint8_t* __restrict__ mask,
-                                                         const float* __restrict__ rot,
-                                                         const float* __restrict__ opac,
-                                                         long long count, float beta,
-                                                         unsigned* tile_cnt,
-                                                         unsigned long long* summary) {
-  __shared__ unsigned warp_cnt[NT / 32];
-  const long long base = (long long)blockIdx.x * TILE;
+// Pre-pass of one tile: its split count (returned to thread 0) and the OR of its flags
+// (returned to every thread's `flags_out` lane 0 of each warp; the caller reduces).
+__device__ __forceinline__ unsigned prepare_tile(const uint8_t* __restrict__ mask,
+                                                 const float* __restrict__ rot,
+                                                 const float* __restrict__ opac, long long count,
+                                                 float beta, long long tile, unsigned* warp_cnt,
+                                                 unsigned& flags_out) {
+  const long long base = tile * TILE;
   unsigned local = 0, flags = 0;
   bool m[PER];
   float4 q[PER];
@@ -103,17 +109,27 @@ __global__ void __launch_bounds__(NT) las_prepare_kernel(const uint8_t* __restri
     if (!(r > 0.0f && r < 1.0f)) flags |= IGS_LAS_BAD_OPACITY;
   }
   unsigned w = __reduce_add_sync(0xffffffffu, local);
-  unsigned f = __reduce_or_sync(0xffffffffu, flags);
-  if (lane_id() == 0) {
-    warp_cnt[threadIdx.x >> 5] = w;
-    if (f) atomicOr(&summary[1], (unsigned long long)f);
-  }
+  flags_out = __reduce_or_sync(0xffffffffu, flags);
+  if (lane_id() == 0) warp_cnt[threadIdx.x >> 5] = w;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned t = 0;
+  unsigned t = 0;
+  if (threadIdx.x == 0)
     for (int k = 0; k < NT / 32; ++k) t += warp_cnt[k];
-    tile_cnt[blockIdx.x] = t;
-  }
+  __syncthreads();  // warp_cnt is reused by the next tile
+  return t;
+}
+
+__global__ void __launch_bounds__(NT) las_prepare_kernel(const uint8_t* __restrict__ mask,
+                                                         const float* __restrict__ rot,
+                                                         const float* __restrict__ opac,
+                                                         long long count, float beta,
+                                                         unsigned* tile_cnt,
+                                                         unsigned long long* summary) {
+  __shared__ unsigned warp_cnt[NT / 32];
+  unsigned f = 0;
+  const unsigned t = prepare_tile(mask, rot, opac, count, beta, blockIdx.x, warp_cnt, f);
+  if (lane_id() == 0 && f) atomicOr(&summary[1], (unsigned long long)f);
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = t;
 }
 
 // Single block: exclusive scan of the tile counts; summary[0] = total.
@@ -135,10 +151,9 @@ __global__ void __launch_bounds__(1024) las_scan_kernel(const unsigned* tile_cnt
 
 // Clone the SH rows (Q4 float4 each) of a tile's compacted parents src_idx[0..n) to the
 // consecutive appended rows slot0 ..: 16-byte streaming loads, U in flight per thread.
-template <int Q4>
+template <int Q4, int U>
 __device__ __forceinline__ void clone_rows(float* sh, const long long* src_idx, unsigned n,
                                            unsigned long long slot0) {
-  constexpr int U = 8;
   const float4* src = reinterpret_cast<const float4*>(sh);
   float4* dstp = reinterpret_cast<float4*>(sh);
   const unsigned total = n * Q4;
@@ -158,35 +173,31 @@ __device__ __forceinline__ void clone_rows(float* sh, const long long* src_idx, 
   }
 }
 
-// Fused split (igs_las_split / igs_las2d_split): the apply pass runs right behind the
-// pre-pass and reads its summary {n_split, flags} itself; any error the host will raise
-// (BudgetError, or a flagged domain error) makes every block return before writing, so the
-// scene is untouched exactly as when the host checks first.
-__device__ __forceinline__ bool split_guard(const unsigned long long* guard, long long count,
-                                            long long capacity, unsigned long long bad) {
-  const unsigned long long ns = guard[0], fl = guard[1];
-  return ns != 0 && (unsigned long long)count + ns <= (unsigned long long)capacity && !(fl & bad);
-}
-
 struct Consts {
   float alpha, log_alpha, log_gamma, beta;
 };
 
-__global__ void __launch_bounds__(NT) las_apply_kernel(
-    float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ rot,
-    float* __restrict__ opac, float* __restrict__ sh, long long sh_floats, long long count,
-    const uint8_t* __restrict__ mask, Consts c, int renorm,
-    const unsigned long long* __restrict__ tile_off, const unsigned long long* guard,
-    long long capacity) {
-  __shared__ unsigned warp_cnt[PER * NT / 32];
-  __shared__ unsigned warp_pre[PER * NT / 32];
-  __shared__ long long src_idx[TILE];
-  if (guard) {  // fused split: the pre-pass summary decides on the device (see split_guard)
-    if (!split_guard(guard, count, capacity, IGS_LAS_BAD_QUAT | IGS_LAS_BAD_OPACITY)) return;
-    renorm = (guard[1] & IGS_LAS_RENORM) != 0;
-  }
-  __shared__ unsigned s_total;
-  const long long base = (long long)blockIdx.x * TILE;
+struct TileSmem {
+  unsigned warp_cnt[SUBS];
+  unsigned warp_pre[SUBS];
+  long long src_idx[TILE];
+  unsigned total;
+};
+
+// Split pass of one 3-D tile whose appended children start at slot0 (= count + the number
+// of masked parents before the tile).
+template <int CLONE_U>
+__device__ __forceinline__ void apply_tile3(float* __restrict__ pos, float* __restrict__ ls,
+                                            float* __restrict__ rot, float* __restrict__ opac,
+                                            float* __restrict__ sh, long long sh_floats,
+                                            long long count, const uint8_t* __restrict__ mask,
+                                            const Consts& c, int renorm, long long tile,
+                                            unsigned long long slot0, TileSmem& ts) {
+  unsigned* warp_cnt = ts.warp_cnt;
+  unsigned* warp_pre = ts.warp_pre;
+  long long* src_idx = ts.src_idx;
+  unsigned& s_total = ts.total;
+  const long long base = tile * TILE;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   bool m[PER];
   unsigned wrank[PER];
@@ -211,7 +222,6 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
     if (threadIdx.x == 31) s_total = x;
   }
   __syncthreads();
-  const unsigned long long slot0 = (unsigned long long)count + tile_off[blockIdx.x];
 
   // every load of the thread's parents first (one memory latency), then the arithmetic
   float lv[PER][3], pv[PER][3], ov[PER];
@@ -299,9 +309,9 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
   const unsigned n = s_total;
   if (n == 0 || sh_floats == 0) return;
   if (sh_floats == 48) {  // SH degree 3: 12 float4 per row, four loads in flight per thread
-    clone_rows<12>(sh, src_idx, n, slot0);
+    clone_rows<12, CLONE_U>(sh, src_idx, n, slot0);
   } else if (sh_floats == 12) {  // SH degree 1
-    clone_rows<3>(sh, src_idx, n, slot0);
+    clone_rows<3, CLONE_U>(sh, src_idx, n, slot0);
   } else if ((sh_floats & 3) == 0) {
     const long long q4 = sh_floats >> 2;
     const float4* src = reinterpret_cast<const float4*>(sh);
@@ -321,17 +331,46 @@ __global__ void __launch_bounds__(NT) las_apply_kernel(
   }
 }
 
+// guard (fused split): the pre-pass summary {n_split, flags} in device memory; the apply
+// returns without writing when the host is about to raise (split_guard), and renormalises
+// per its RENORM flag.
+__device__ __forceinline__ bool split_guard(const unsigned long long* guard, long long count,
+                                            long long capacity, unsigned long long bad) {
+  const unsigned long long ns = guard[0], fl = guard[1];
+  return ns != 0 && (unsigned long long)count + ns <= (unsigned long long)capacity && !(fl & bad);
+}
+
+__global__ void __launch_bounds__(NT) las_apply_kernel(
+    float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ rot,
+    float* __restrict__ opac, float* __restrict__ sh, long long sh_floats, long long count,
+    const uint8_t* __restrict__ mask, Consts c, int renorm,
+    const unsigned long long* __restrict__ tile_off, const unsigned long long* guard,
+    long long capacity) {
+  __shared__ TileSmem ts;
+  if (guard) {
+    if (!split_guard(guard, count, capacity, IGS_LAS_BAD_QUAT | IGS_LAS_BAD_OPACITY)) return;
+    renorm = (guard[1] & IGS_LAS_RENORM) != 0;
+  }
+  apply_tile3<8>(pos, ls, rot, opac, sh, sh_floats, count, mask, c, renorm, blockIdx.x,
+              (unsigned long long)count + tile_off[blockIdx.x], ts);
+}
+
 // 2-D Long-Axis-Split (las_split.py:109-117, 182-197): the same slot rule and scale/opacity
 // update; the displacement is column l of [[cos, -sin], [sin, cos]] (theta float32).
-__global__ void __launch_bounds__(NT) las2d_apply_kernel(
-    float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ theta,
-    float* __restrict__ opac, float* __restrict__ col, long long count,
-    const uint8_t* __restrict__ mask, Consts c, const unsigned long long* __restrict__ tile_off,
-    const unsigned long long* guard, long long capacity) {
-  __shared__ unsigned warp_cnt[PER * NT / 32];
-  __shared__ unsigned warp_pre[PER * NT / 32];
-  if (guard && !split_guard(guard, count, capacity, IGS_LAS_BAD_OPACITY)) return;
-  const long long base = (long long)blockIdx.x * TILE;
+struct TileSmem2 {
+  unsigned warp_cnt[SUBS];
+  unsigned warp_pre[SUBS];
+};
+
+__device__ __forceinline__ void apply_tile2(float* __restrict__ pos, float* __restrict__ ls,
+                                            float* __restrict__ theta, float* __restrict__ opac,
+                                            float* __restrict__ col, long long count,
+                                            const uint8_t* __restrict__ mask, const Consts& c,
+                                            long long tile, unsigned long long slot0,
+                                            TileSmem2& ts) {
+  unsigned* warp_cnt = ts.warp_cnt;
+  unsigned* warp_pre = ts.warp_pre;
+  const long long base = tile * TILE;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   bool m[PER];
   unsigned wrank[PER];
@@ -355,7 +394,6 @@ __global__ void __launch_bounds__(NT) las2d_apply_kernel(
     if (threadIdx.x < (unsigned)SUBS) warp_pre[threadIdx.x] = x - v;
   }
   __syncthreads();
-  const unsigned long long slot0 = (unsigned long long)count + tile_off[blockIdx.x];
   // every load of the thread's parents first, then the arithmetic (as the 3-D pass)
   float lv[PER][2], pv[PER][2], ov[PER], tv[PER], cv[PER][3];
 #pragma unroll
@@ -409,6 +447,133 @@ __global__ void __launch_bounds__(NT) las2d_apply_kernel(
     col[3 * dst + 1] = cv[j][1];
     col[3 * dst + 2] = cv[j][2];
   }
+}
+
+__global__ void __launch_bounds__(NT) las2d_apply_kernel(
+    float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ theta,
+    float* __restrict__ opac, float* __restrict__ col, long long count,
+    const uint8_t* __restrict__ mask, Consts c, const unsigned long long* __restrict__ tile_off,
+    const unsigned long long* guard, long long capacity) {
+  __shared__ TileSmem2 ts;
+  if (guard && !split_guard(guard, count, capacity, IGS_LAS_BAD_OPACITY)) return;
+  apply_tile2(pos, ls, theta, opac, col, count, mask, c, blockIdx.x,
+              (unsigned long long)count + tile_off[blockIdx.x], ts);
+}
+
+// ------------------------------------------------------------ fused split
+// igs_las_split / igs_las2d_split = las_prepare_coop_kernel + the guarded apply kernel, back to
+// back on the stream with no host round trip and no memset:
+//   las_prepare_coop_kernel  one cooperative launch, each CTA owning a contiguous range of
+//     tiles.  Phase 1: the pre-pass of its tiles (tile counts; the CTA's total and flags to its
+//     own slot, so no zero-initialised memory).  Grid barrier.  Phase 2: every CTA reads all CTA
+//     totals / flags, writes the slot offsets of its tiles, and CTA 0 writes the summary
+//     {n_split, flags} to the workspace (the apply's guard) and to the caller's summary.
+//   las_apply_kernel / las2d_apply_kernel with that guard: every block returns before writing
+//     when the host is about to raise, so the scene is untouched as in the reference.
+template <bool D3>
+__global__ void __launch_bounds__(NT) las_prepare_coop_kernel(
+    const uint8_t* __restrict__ mask, const float* __restrict__ rot,
+    const float* __restrict__ opac, long long count, float beta, long long tiles,
+    unsigned* tile_cnt, unsigned long long* tile_off, unsigned long long* cta_tot,
+    unsigned* cta_flag, unsigned long long* guard, int64_t* summary) {
+  __shared__ unsigned warp_cnt[NT / 32];
+  __shared__ unsigned red[NT / 32];
+  __shared__ unsigned long long s_pre, s_tot;
+  __shared__ unsigned s_flags;
+  const long long G = gridDim.x, b = blockIdx.x;
+  const long long t0 = b * tiles / G, t1 = (b + 1) * tiles / G;
+  unsigned long long tot = 0;
+  unsigned flags = 0;
+  for (long long t = t0; t < t1; ++t) {
+    unsigned f = 0;
+    const unsigned n = prepare_tile(mask, D3 ? rot : nullptr, opac, count, beta, t, warp_cnt, f);
+    flags |= f;
+    if (threadIdx.x == 0) {
+      tile_cnt[t] = n;
+      tot += n;
+    }
+  }
+  if (lane_id() == 0) red[threadIdx.x >> 5] = flags;
+  if (threadIdx.x == 0) {
+    s_pre = 0;
+    s_tot = 0;
+    s_flags = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned f = 0;
+    for (int k = 0; k < NT / 32; ++k) f |= red[k];
+    cta_tot[b] = tot;
+    cta_flag[b] = f;
+  }
+  cooperative_groups::this_grid().sync();
+  unsigned long long pre = 0, all = 0;
+  unsigned fl = 0;
+  for (long long k = threadIdx.x; k < G; k += NT) {
+    const unsigned long long v = __ldcg(&cta_tot[k]);
+    all += v;
+    if (k < b) pre += v;
+    fl |= __ldcg(&cta_flag[k]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pre += __shfl_down_sync(0xffffffffu, pre, o);
+    all += __shfl_down_sync(0xffffffffu, all, o);
+  }
+  fl = __reduce_or_sync(0xffffffffu, fl);
+  if (lane_id() == 0) {
+    atomicAdd(&s_pre, pre);
+    atomicAdd(&s_tot, all);
+    atomicOr(&s_flags, fl);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long off = s_pre;
+    for (long long t = t0; t < t1; ++t) {  // this CTA's own tile counts (a few per CTA)
+      tile_off[t] = off;
+      off += __ldcg(&tile_cnt[t]);
+    }
+    if (b == 0) {
+      guard[0] = s_tot;
+      guard[1] = s_flags;
+      summary[0] = (int64_t)s_tot;
+      summary[1] = (int64_t)s_flags;
+    }
+  }
+}
+
+template <bool D3>
+int launch_prepare_coop(const uint8_t* mask, const float* rot, const float* opac, long long count,
+                        float beta, void* workspace, size_t workspace_bytes, int64_t* summary,
+                        cudaStream_t s, const unsigned long long** guard_out,
+                        const unsigned long long** tile_off_out) {
+  Layout L = layout(count);
+  if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
+  char* w = (char*)workspace;
+  const long long tiles = (count + TILE - 1) / TILE;
+  static int per_sm[2] = {-1, -1};
+  int& bps = per_sm[D3 ? 1 : 0];
+  if (bps < 0) {
+    int n = 0;
+    IGS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, las_prepare_coop_kernel<D3>, NT, 0));
+    bps = n;
+  }
+  long long grid = (long long)bps * sm_count();
+  if (grid > MAX_CTAS) grid = MAX_CTAS;
+  if (grid > tiles) grid = tiles;
+  if (grid < 1) return IGS_ERR_CUDA;
+  unsigned* tile_cnt = (unsigned*)(w + L.tile_cnt);
+  unsigned long long* tile_off = (unsigned long long*)(w + L.tile_off);
+  unsigned long long* cta_tot = (unsigned long long*)(w + L.cta_tot);
+  unsigned* cta_flag = (unsigned*)(w + L.cta_flag);
+  unsigned long long* guard = (unsigned long long*)(w + L.guard);
+  void* args[] = {&mask, &rot, &opac, &count, &beta, (void*)&tiles, &tile_cnt, &tile_off,
+                  &cta_tot, &cta_flag, &guard, &summary};
+  IGS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)las_prepare_coop_kernel<D3>,
+                                           dim3((unsigned)grid), dim3(NT), args, 0, s));
+  *guard_out = guard;
+  *tile_off_out = tile_off;
+  return IGS_OK;
 }
 
 }  // namespace las
@@ -491,22 +656,26 @@ int igs_las_split(float* positions, float* log_scales, float* rotations, float* 
                   float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
                   const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,
                   void* workspace, size_t workspace_bytes, int64_t* summary, void* stream) {
-  if (count < 0 || capacity < count || sh_floats < 0) return IGS_ERR_ARGUMENT;
-  if (count > 0 && (!positions || !log_scales || !rotations || !opacity_logits))
+  if (count < 0 || capacity < count || sh_floats < 0 || !summary) return IGS_ERR_ARGUMENT;
+  if (count > 0 && (!positions || !log_scales || !rotations || !opacity_logits || !mask))
     return IGS_ERR_ARGUMENT;
   if (sh_floats > 0 && count > 0 && !sh) return IGS_ERR_ARGUMENT;
   if (((uintptr_t)rotations & 15) || (sh_floats % 4 == 0 && ((uintptr_t)sh & 15)))
     return IGS_ERR_ARGUMENT;
-  int st = igs_las_prepare(mask, rotations, opacity_logits, count, beta, workspace,
-                           workspace_bytes, summary, stream);
-  if (st != IGS_OK || count == 0) return st;
-  las::Layout L = las::layout(count);
-  long long tiles = (count + las::TILE - 1) / las::TILE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (count == 0) {
+    IGS_CUDA_TRY(cudaMemsetAsync(summary, 0, 2 * sizeof(int64_t), s));
+    return IGS_OK;
+  }
+  const unsigned long long *guard = nullptr, *tile_off = nullptr;
+  int st = las::launch_prepare_coop<true>(mask, rotations, opacity_logits, count, beta, workspace,
+                                          workspace_bytes, summary, s, &guard, &tile_off);
+  if (st != IGS_OK) return st;
+  const long long tiles = (count + las::TILE - 1) / las::TILE;
   las::Consts c{alpha, log_alpha, log_gamma, beta};
-  las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
+  las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
       positions, log_scales, rotations, opacity_logits, sh, sh_floats, count, mask, c, 0,
-      (const unsigned long long*)((char*)workspace + L.tile_off),
-      (const unsigned long long*)summary, capacity);
+      tile_off, guard, capacity);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }
@@ -515,19 +684,23 @@ int igs_las2d_split(float* positions, float* log_scales, float* thetas, float* o
                     float* colors, int64_t count, int64_t capacity, const uint8_t* mask,
                     float alpha, float log_alpha, float log_gamma, float beta, void* workspace,
                     size_t workspace_bytes, int64_t* summary, void* stream) {
-  if (count < 0 || capacity < count) return IGS_ERR_ARGUMENT;
-  if (count > 0 && (!positions || !log_scales || !thetas || !opacity_logits || !colors))
+  if (count < 0 || capacity < count || !summary) return IGS_ERR_ARGUMENT;
+  if (count > 0 && (!positions || !log_scales || !thetas || !opacity_logits || !colors || !mask))
     return IGS_ERR_ARGUMENT;
-  int st = igs_las_prepare(mask, nullptr, opacity_logits, count, beta, workspace,
-                           workspace_bytes, summary, stream);
-  if (st != IGS_OK || count == 0) return st;
-  las::Layout L = las::layout(count);
-  long long tiles = (count + las::TILE - 1) / las::TILE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (count == 0) {
+    IGS_CUDA_TRY(cudaMemsetAsync(summary, 0, 2 * sizeof(int64_t), s));
+    return IGS_OK;
+  }
+  const unsigned long long *guard = nullptr, *tile_off = nullptr;
+  int st = las::launch_prepare_coop<false>(mask, nullptr, opacity_logits, count, beta, workspace,
+                                           workspace_bytes, summary, s, &guard, &tile_off);
+  if (st != IGS_OK) return st;
+  const long long tiles = (count + las::TILE - 1) / las::TILE;
   las::Consts c{alpha, log_alpha, log_gamma, beta};
-  las::las2d_apply_kernel<<<(unsigned)tiles, las::NT, 0, (cudaStream_t)stream>>>(
-      positions, log_scales, thetas, opacity_logits, colors, count, mask, c,
-      (const unsigned long long*)((char*)workspace + L.tile_off),
-      (const unsigned long long*)summary, capacity);
+  las::las2d_apply_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
+      positions, log_scales, thetas, opacity_logits, colors, count, mask, c, tile_off, guard,
+      capacity);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }

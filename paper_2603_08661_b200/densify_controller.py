@@ -185,10 +185,12 @@ def densify_step(scene, stats: DensifyStats, cfg: DensifyConfig, step: int) -> D
     c = cfg.split_constants
     if take_cap > 0:
         # select, then the fused split (pre-pass + device-guarded apply); one host read
-        res = torch.empty(4, dtype=torch.int64, device=stats._device)  # counts | split summary
+        # counts | split summary, written by the kernels straight into pinned host memory
+        res, view = _las.pinned_summary(stats._device, 4)
         mask, _ = _launch_select(stats, cfg, step, take_cap, counts=res[:2])
         _las.split_async(scene, mask.view(torch.bool), c, summary=res[2:])
-        eligible, _, n_split, flags = res.cpu().tolist()
+        _las.sync(stats._device)
+        eligible, n_split, flags = int(view[0]), int(view[2]), int(view[3])
         _las.finish_split(scene, n_split, flags)
     else:
         eligible, n_split = eligible_count(stats, cfg, step), 0

@@ -6,8 +6,12 @@ overwritten in place by their +offset child, the -offset children are appended
 in ascending parent order, ``BudgetError`` / ``ValueError`` are raised before
 anything is written, an all-false mask leaves the scene untouched.
 
-Device flow: ``igs_las_prepare`` (mask scan + batch flags) -> one 16-byte
-device->host read of {n_split, flags} -> host checks -> ``igs_las_apply``.
+Device flow of ``las_split_batch``: ``igs_las_split`` -- one cooperative launch
+(pre-pass, grid barrier, device-guarded apply) that writes {n_split, flags}
+straight into a pinned host buffer -> stream synchronise -> host checks raise
+the reference's errors (the device wrote nothing in that case) or grow the count.
+The sharded path keeps the two-call form (``igs_las_prepare`` -> global checks
+-> ``igs_las_apply``).
 """
 
 from __future__ import annotations
@@ -56,6 +60,9 @@ def _device_constants(alpha, gamma_axis, beta):
 
 
 def _mask_tensor(mask, n, device):
+    if (type(mask) is torch.Tensor and mask.dtype is torch.bool and mask.ndim == 1
+            and mask.shape[0] == n and mask.is_contiguous() and mask.device == device):
+        return mask.view(torch.uint8)  # the common case: no copy, no conversion
     if isinstance(mask, torch.Tensor):
         m = mask.to(device)
     else:
@@ -113,11 +120,44 @@ def check_and_apply(prep: _Prepared, n_split: int, flags: int, c: SplitConstants
     return scene.count
 
 
+_pinned: dict = {}
+
+
+def pinned_summary(device, n=2):
+    """A reusable page-locked int64[n] (per device and stream) that kernels write directly
+    (host memory is device-accessible under unified addressing), with a numpy view for the
+    host read after the stream synchronises: no device->host copy call per split."""
+    device = torch.device(device)
+    key = (device.index, _lib.stream_handle(device), n)
+    hit = _pinned.get(key)
+    if hit is None:
+        t = torch.zeros(n, dtype=torch.int64, pin_memory=True)
+        hit = _pinned[key] = (t, t.numpy())
+    return hit
+
+
+def sync(device):
+    """Wait for the current stream of `device` (one C call on the raw stream handle)."""
+    _lib.check(_lib.lib().igs_stream_synchronize(_lib.stream_handle(device)), "synchronize")
+
+
+def _column_ptrs(scene):
+    """The scene's column pointers for the C calls, cached on the scene and rebuilt whenever a
+    column buffer was replaced (capacity growth re-reserves the buffers)."""
+    bufs = tuple(getattr(scene, a) for a in scene._buffers)
+    hit = scene.__dict__.get("_las_ptrs")
+    if hit is None or any(x is not y for x, y in zip(hit[0], bufs)):
+        hit = (bufs, tuple(b.data_ptr() for b in bufs))
+        scene.__dict__["_las_ptrs"] = hit
+    return hit[1]
+
+
 def split_async(scene, mask, c: SplitConstants, summary=None):
-    """Launch the fused split (igs_las_split / igs_las2d_split): the pre-pass, then the apply
-    pass guarded on the device by the pre-pass summary, with no host round trip between them.
-    Returns the summary (device int64[2] = {n_split, flags}; written into ``summary`` when
-    given), not yet read."""
+    """Launch the fused split (igs_las_split / igs_las2d_split): ONE cooperative launch that
+    runs the pre-pass, a grid barrier, and the apply pass guarded on the device by the
+    pre-pass totals, with no host round trip in between.  Returns the summary int64[2] =
+    {n_split, flags} (written into ``summary`` when given: device memory or pinned host
+    memory), not yet read."""
     L = _lib.lib()
     m = _mask_tensor(mask, scene.count, scene.device)
     nbytes = _lib.query_size(L.igs_las_workspace_bytes, scene.count)
@@ -125,13 +165,13 @@ def split_async(scene, mask, c: SplitConstants, summary=None):
     if summary is None:
         summary = torch.empty(2, dtype=torch.int64, device=scene.device)
     alpha, log_alpha, log_gamma, beta = c.device_constants()
+    stream = _lib.stream_handle(scene.device)
     if isinstance(scene, Scene3):
-        _lib.check(L.igs_las_split(scene._pos.data_ptr(), scene._ls.data_ptr(),
-                                   scene._rot.data_ptr(), scene._op.data_ptr(),
-                                   scene._sh.data_ptr(), scene._sh.shape[1] * 3, scene.count,
+        pos, ls, rot, op, sh = _column_ptrs(scene)
+        _lib.check(L.igs_las_split(pos, ls, rot, op, sh, scene._sh.shape[1] * 3, scene.count,
                                    scene.capacity, m.data_ptr(), alpha, log_alpha, log_gamma,
                                    beta, ws.data_ptr(), ws.numel(), summary.data_ptr(),
-                                   _lib.stream_handle()), "las_split_batch")
+                                   stream), "las_split_batch")
     else:
         cols = scene._cols
         _lib.check(L.igs_las2d_split(cols["positions"].data_ptr(), cols["log_scales"].data_ptr(),
@@ -139,7 +179,7 @@ def split_async(scene, mask, c: SplitConstants, summary=None):
                                      cols["colors"].data_ptr(), scene.count, scene.capacity,
                                      m.data_ptr(), alpha, log_alpha, log_gamma, beta,
                                      ws.data_ptr(), ws.numel(), summary.data_ptr(),
-                                     _lib.stream_handle()), "las_split_batch_2d")
+                                     stream), "las_split_batch_2d")
     return summary
 
 
@@ -163,9 +203,13 @@ def las_split_batch(scene: Scene3, mask, c: SplitConstants = SplitConstants()) -
     """Split every masked primitive of a GPU scene in place (las_split.py:158-179)."""
     if not isinstance(scene, Scene3):
         raise TypeError(f"expected a paper_2603_08661_b200.core.Scene3, got {type(scene).__name__}")
-    summary = split_async(scene, mask, c)
-    n_split, flags = (int(v) for v in summary.cpu().tolist())
-    finish_split(scene, n_split, flags)
+    if scene.count == 0:
+        _mask_tensor(mask, 0, scene.device)  # the length check; nothing to split
+        return scene.validate()
+    buf, view = pinned_summary(scene.device)
+    split_async(scene, mask, c, summary=buf)
+    sync(scene.device)
+    finish_split(scene, int(view[0]), int(view[1]))
     return scene.validate()
 
 
@@ -181,7 +225,11 @@ def las_split_batch_2d(scene: Scene2, mask, c: SplitConstants = SplitConstants()
     parents take the +offset child in place, -offset children are appended in parent order."""
     if not isinstance(scene, Scene2):
         raise TypeError(f"expected a paper_2603_08661_b200.core.Scene2, got {type(scene).__name__}")
-    summary = split_async(scene, mask, c)
-    n_split, flags = (int(v) for v in summary.cpu().tolist())
-    finish_split(scene, n_split, flags)
+    if scene.count == 0:
+        _mask_tensor(mask, 0, scene.device)
+        return scene.validate()
+    buf, view = pinned_summary(scene.device)
+    split_async(scene, mask, c, summary=buf)
+    sync(scene.device)
+    finish_split(scene, int(view[0]), int(view[1]))
     return scene.validate()
