@@ -19,6 +19,10 @@ from .las_split import (BudgetError, SplitConstants, las_split_batch, las_split_
                         principal_axis)
 from .scene_io import (BadMagicError, FormatError, SceneFormatError, SizeMismatchError,
                        UnsupportedVersionError, read_scene, scene_bytes, write_scene)
-from .schedule import DensifyConfig, is_densify_step, is_warmup_step
+from .schedule import (DensifyConfig, ExpSchedule, default_schedules, is_densify_step,
+                       is_warmup_step, lr_at)
+from .splat2d import (RenderParams, TrainConfig, TrainResult, backward,
+                      desk_scale_densify_config, loss_l2, psnr, render, ssim, train)
+from .io_cli import read_image, write_image
 
 __version__ = "0.1.0"

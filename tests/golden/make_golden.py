@@ -4,7 +4,8 @@ Usage (build container only -- ``/root/reference`` does not exist on the GPU box
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
 
-Writes ``tests/golden/{edge,nms,median,las,select}.npz``.  The fixtures are
+Writes ``tests/golden/{edge,nms,median,las,select,sample,las2d,igsp,splat2d,cli}.npz``
+(``make_golden.py NAME ...`` regenerates only those).  The fixtures are
 small (<= 128x128 images, <= 2k Gaussians) and committed; tests compare the
 oracle against them on CPU and the CUDA path against them on the GPU.
 """
@@ -424,10 +425,93 @@ def igsp_cases():
     return out
 
 
+def square_target(w=64, h=64):
+    """pkg/tests/conftest.py:5-13."""
+    yy, xx = np.mgrid[0:h, 0:w]
+    t = np.zeros((h, w, 3))
+    t[..., 0] = xx / (w - 1) * 0.4
+    t[..., 1] = 0.15
+    t[..., 2] = yy / (h - 1) * 0.4
+    t[16:38, 12:34] = 1.0
+    return t
+
+
+def splat2d_cases():
+    """The reference trainer's forward/backward (splat2d.py:153-218) on random scenes, and a
+    short seeded training run (splat2d.py:373-403) for the trajectory comparison."""
+    from splitkit.splat2d import RenderParams, TrainConfig, _loss_and_grads, render, train
+    out = {}
+    rng = np.random.default_rng(77)
+    targets = {"square": square_target(), "synth": synth_view(20, 24, 5)}
+    k = 0
+    for tname, tgt in targets.items():
+        h, w = tgt.shape[:2]
+        for n in (1, 7, 40):
+            pos = np.stack([rng.uniform(-2, w + 1, n), rng.uniform(-2, h + 1, n)], 1)
+            ls = rng.uniform(0.0, 2.0, (n, 2))
+            th = rng.uniform(-3, 3, n)
+            op = rng.normal(0, 1.5, n)
+            col = rng.random((n, 3))
+            sc = Scene2(pos, ls, th, op, col, capacity=n)
+            p = RenderParams(width=w, height=h, footprint_cutoff=3.0 if k % 2 == 0 else 2.0)
+            loss, image, g = _loss_and_grads(sc, tgt, p)
+            key = f"c{k}"
+            out[f"{key}/target"] = tgt
+            out[f"{key}/cutoff"] = np.array(p.footprint_cutoff)
+            for name in ("positions", "log_scales", "thetas", "opacity_logits", "colors"):
+                out[f"{key}/{name}"] = getattr(sc, name)
+                out[f"{key}/grad_{name}"] = getattr(g, name)
+            out[f"{key}/loss"] = np.array(loss)
+            out[f"{key}/image"] = image
+            out[f"{key}/render"] = render(sc, p)
+            k += 1
+    res = train(square_target(), TrainConfig(total_iters=120, seed=0, n_init=8, budget=32))
+    out["run/trace"] = np.array([r[:2] + r[3:4] for r in res.trace], dtype=np.float64)
+    out["run/events"] = np.array([[e.step, e.eligible, e.split, e.count_after]
+                                  for e in res.events], dtype=np.int64)
+    out["run/final_psnr"] = np.array(res.final_psnr)
+    return out
+
+
+def cli_cases():
+    """The reference CLI (io_cli.py:315-349) on small files: input and output bytes."""
+    import tempfile
+    from splitkit.io_cli import main as cli_main
+    from splitkit.io_cli import write_image, write_scene
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        img = synth_view(40, 52, 9)
+        write_image(os.path.join(d, "in.ppm"), img)
+        out["edge/in_ppm"] = np.frombuffer(open(os.path.join(d, "in.ppm"), "rb").read(), np.uint8)
+        for tag, flags in (("default", []), ("no_nms", ["--no-nms"]),
+                           ("no_median", ["--no-median"]), ("sigma2", ["--sigma", "2.0"])):
+            rc = cli_main(["edge-map", "--input", os.path.join(d, "in.ppm"), "--output",
+                           os.path.join(d, "o.pgm"), *flags])
+            assert rc == 0
+            out[f"edge/{tag}"] = np.frombuffer(open(os.path.join(d, "o.pgm"), "rb").read(),
+                                               np.uint8)
+        rng = np.random.default_rng(31)
+        sc = random_scene(rng, 50, 50)
+        write_scene(sc, os.path.join(d, "s.igsp"))
+        out["split/in"] = np.frombuffer(open(os.path.join(d, "s.igsp"), "rb").read(), np.uint8)
+        rc = cli_main(["split", "--scene", os.path.join(d, "s.igsp"), "--mask", "0,3,7,49",
+                       "--out", os.path.join(d, "o.igsp")])
+        assert rc == 0
+        out["split/out"] = np.frombuffer(open(os.path.join(d, "o.igsp"), "rb").read(), np.uint8)
+        rc = cli_main(["split", "--scene", os.path.join(d, "s.igsp"), "--mask", "1,2",
+                       "--budget", "51", "--out", os.path.join(d, "o2.igsp")])
+        out["split/budget_rc"] = np.array(rc)
+    return out
+
+
 def main():
+    only = sys.argv[1:]
     for name, fn in (("edge", edge_cases), ("nms", nms_cases), ("median", median_cases),
                      ("las", las_cases), ("select", select_cases), ("sample", sample_cases),
-                     ("las2d", las2d_cases), ("igsp", igsp_cases)):
+                     ("las2d", las2d_cases), ("igsp", igsp_cases), ("splat2d", splat2d_cases),
+                     ("cli", cli_cases)):
+        if only and name not in only:
+            continue
         data = fn()
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **data)
         print(name, len(data), "arrays")
