@@ -799,8 +799,9 @@ def bench_uhd(args, world, dev, peak):
 def bench_densify_sharded(args, world, rank, dev):
     """BASELINE.json configs[3]: the full densify step on a 6M-Gaussian SH3 cloud split in
     contiguous shards over the ranks (strong scaling: 6M total at every N).  One step =
-    sharded select (4 histogram all-reduces + 1 tie all-gather over NCCL) + sharded LAS
-    (1 all-gather of counts/flags) + the host reads; max over ranks of the median step."""
+    keys + one 256 KB histogram all-reduce + boundary records all-gather + finalize + the
+    guarded split of each shard + one host read of the plan; max over ranks of the median
+    step."""
     import torch
 
     import paper_2603_08661_b200 as igs
@@ -823,6 +824,7 @@ def bench_densify_sharded(args, world, rank, dev):
         for name, v in pristine.items():
             getattr(scene, name)[:k].copy_(v)
         scene._set_count(k)
+        sharded.detach(scene)   # the restored cloud is again a contiguous shard
         stats = igs.DensifyStats(k, device=dev)
         stats._grad_sum.copy_(grad_t)
         stats._accum_count = 1
@@ -846,7 +848,8 @@ def bench_densify_sharded(args, world, rank, dev):
             "config": {"workload": "densify_step_sharded on a 6M-Gaussian SH3 cloud, contiguous "
                                    f"shards of {k} per GPU, take = ceil(0.05 N) = 300k "
                                    "(BASELINE.json configs[3])",
-                       "collectives": "4 x 256 KB all-reduce + 2 small all-gathers per step "
+                       "collectives": "1 x 256 KB all-reduce + 1 all-gather of 64 KB "
+                                      "boundary records per rank per step "
                                       + ("(NCCL)" if world > 1 else "(none at N=1)")}}
 
 

@@ -133,33 +133,39 @@ int igs_select_candidates(const double* grad_sum, int64_t accum_count, const dou
 int igs_accumulate_grad_norms(double* grad_sum, const void* grads, int dtype, int64_t n,
                               void* stream);
 
-/* ---- sharded selection (multi-GPU) ---------------------- *
- * The same result as igs_select_candidates over the concatenation of every rank's
- * contiguous shard (densify_controller.py:80-106 on the global arrays), split into the
- * per-rank launches of a radix select whose merge steps are collectives the caller issues
- * on the same stream (torch.distributed / NCCL):
- *   igs_select_shard_keys                 -> all-reduce(sum) hist
- *   igs_select_shard_resolve(round 0)
- *   for round 1..3: igs_select_shard_hist -> all-reduce(sum) hist; igs_select_shard_resolve
- *   igs_select_shard_ties                 -> all-gather local_ties (one int64 per rank)
- *   igs_select_shard_finalize
- * hist is a device int32[IGS_SHARD_HIST_LEN] buffer: 65536 digit bins, then the eligible
- * count (round 0).  take_cap is computed on the host from the GLOBAL count and headroom
- * (:99-100).  counts (device int64[2], nullable) receives the global {#eligible, take}. */
+/* ---- sharded densify step (multi-GPU) ------------------- *
+ * select_candidates + las_split_batch of densify_step (densify_controller.py:80-106,
+ * 125-147) over a cloud sharded across ranks, bit-identical to the single-process step on the
+ * reference's global array.  Each row carries its global index gidx (int64; contiguous ranges
+ * before the first split, children appended in the reference's order afterwards); ties break
+ * by gidx.  Per event, all stream-ordered, two collectives, one host read at the end:
+ *   igs_shard_keys        -> all-reduce(sum) hist (int32[IGS_SHARD_HIST_LEN]: 65536 bins of a
+ *                            monotone 16-bit digit of the score key, then the eligible count)
+ *   igs_shard_boundary    resolve take / boundary digit / need, compact this rank's
+ *                            boundary-bucket entries into its record
+ *                         -> all-gather records (int64[4 + 2 record_cap] per rank)
+ *   igs_shard_finalize    threshold (key, gidx) by radix select over every record; the plan
+ *                            (int64[16]) and this rank's mask
+ *   igs_las_split_guarded the split of this shard, guarded by plan[0..1]
+ *   igs_shard_child_index gidx of this rank's appended children
+ * plan words: [0] this rank's split count if the split may go ahead else 0, [1] batch LAS
+ * flags, [2] status (0 ok, 1 nothing selected, 2 boundary bucket larger than record_cap:
+ * nothing split, re-run boundary/gather/finalize with record_cap >= plan[7]), [3] global
+ * split count, [4] global eligible count, [5] global index of this rank's first child,
+ * [6] this rank's split count, [7] largest boundary-bucket count over the ranks. */
 #define IGS_SHARD_HIST_LEN 65537
-int igs_select_shard_workspace_bytes(int64_t n, size_t* bytes);
-int igs_select_shard_keys(const double* grad_sum, int64_t accum_count, const double* edge_score,
-                          int64_t n, double grad_threshold, int warmup, int policy, int32_t* hist,
-                          void* workspace, size_t workspace_bytes, void* stream);
-int igs_select_shard_resolve(const int32_t* global_hist, int round, int64_t take_cap,
-                             void* workspace, size_t workspace_bytes, int64_t* counts,
-                             void* stream);
-int igs_select_shard_hist(int64_t n, int round, int32_t* hist, void* workspace,
-                          size_t workspace_bytes, void* stream);
-int igs_select_shard_ties(int64_t n, int64_t* local_ties, void* workspace, size_t workspace_bytes,
-                          void* stream);
-int igs_select_shard_finalize(int64_t n, const int64_t* all_ties, int rank, uint8_t* mask,
-                              void* workspace, size_t workspace_bytes, void* stream);
+int igs_shard_workspace_bytes(int64_t n, size_t* bytes);
+int igs_shard_keys(const double* grad_sum, int64_t accum_count, const double* edge_score,
+                   int64_t n, double grad_threshold, int warmup, int policy, int32_t* hist,
+                   void* workspace, size_t workspace_bytes, void* stream);
+int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64_t* gidx,
+                       const float* rotations, const float* opacity_logits, float beta,
+                       int64_t n, int64_t record_cap, int64_t* record, void* workspace,
+                       size_t workspace_bytes, void* stream);
+int igs_shard_finalize(const int64_t* records, int world, int rank, int64_t record_cap,
+                       int64_t n_global, const int64_t* gidx, int64_t n, uint8_t* mask,
+                       int64_t* plan, void* workspace, size_t workspace_bytes, void* stream);
+int igs_shard_child_index(int64_t* gidx, int64_t count, const int64_t* plan, void* stream);
 
 /* ---- Long-Axis-Split (las_split.py:146-179) ----------------------------- */
 
@@ -210,6 +216,17 @@ int igs_las2d_split(float* positions, float* log_scales, float* thetas, float* o
                     float* colors, int64_t count, int64_t capacity, const uint8_t* mask,
                     float alpha, float log_alpha, float log_gamma, float beta, void* workspace,
                     size_t workspace_bytes, int64_t* summary, void* stream);
+
+/* The split of one shard under the sharded step's plan: the pre-pass for this shard's slot
+ * offsets, then the apply pass guarded by the device words guard = {n_split or 0, batch
+ * flags} against reserved_rows.  dims 3: rotations (cap,4), sh_or_colors = sh (cap,
+ * sh_floats); dims 2: rotations = thetas (cap,), sh_or_colors = colors (cap,3). */
+int igs_las_split_guarded(float* positions, float* log_scales, float* rotations,
+                          float* opacity_logits, float* sh_or_colors, int64_t sh_floats,
+                          int dims, int64_t count, int64_t reserved_rows, const uint8_t* mask,
+                          float alpha, float log_alpha, float log_gamma, float beta,
+                          const int64_t* guard, void* workspace, size_t workspace_bytes,
+                          void* stream);
 
 /* ---- scene files (io_cli.py:83-134) ------------------------------------- */
 

@@ -48,12 +48,13 @@ SIGNATURES = {
     "igs_select_candidates": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _i64, _vp, _vp, _vp,
                                      _sz, _vp]),
     "igs_accumulate_grad_norms": (_int, [_vp, _vp, _int, _i64, _vp]),
-    "igs_select_shard_workspace_bytes": (_int, [_i64, _szp]),
-    "igs_select_shard_keys": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _vp, _vp, _sz, _vp]),
-    "igs_select_shard_resolve": (_int, [_vp, _int, _i64, _vp, _sz, _vp, _vp]),
-    "igs_select_shard_hist": (_int, [_i64, _int, _vp, _vp, _sz, _vp]),
-    "igs_select_shard_ties": (_int, [_i64, _vp, _vp, _sz, _vp]),
-    "igs_select_shard_finalize": (_int, [_i64, _vp, _int, _vp, _vp, _sz, _vp]),
+    "igs_shard_workspace_bytes": (_int, [_i64, _szp]),
+    "igs_shard_keys": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _vp, _vp, _sz, _vp]),
+    "igs_shard_boundary": (_int, [_vp, _i64, _vp, _vp, _vp, _flt, _i64, _i64, _vp, _vp, _sz,
+                                  _vp]),
+    "igs_shard_finalize": (_int, [_vp, _int, _int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _sz,
+                                  _vp]),
+    "igs_shard_child_index": (_int, [_vp, _i64, _vp, _vp]),
     "igs_las_workspace_bytes": (_int, [_i64, _szp]),
     "igs_las_prepare": (_int, [_vp, _vp, _vp, _i64, _flt, _vp, _sz, _vp, _vp]),
     "igs_las_apply": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt, _flt,
@@ -64,6 +65,8 @@ SIGNATURES = {
                                _vp, _sz, _vp, _vp]),
     "igs_las2d_apply": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _flt, _flt, _flt, _flt,
                                _vp, _sz, _vp]),
+    "igs_las_split_guarded": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _int, _i64, _i64, _vp, _flt,
+                                     _flt, _flt, _flt, _vp, _vp, _sz, _vp]),
 }
 
 _lib = None

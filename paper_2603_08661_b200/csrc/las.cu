@@ -705,4 +705,47 @@ int igs_las2d_split(float* positions, float* log_scales, float* thetas, float* o
   return IGS_OK;
 }
 
+// The split of one shard under a decision taken elsewhere (the sharded densify step): the
+// cooperative pre-pass for this shard's slot offsets, then the apply pass guarded by the
+// device words guard = {n_split or 0, batch flags} (RENORM / domain flags over every rank's
+// selected parents) against the shard's reserved rows.
+int igs_las_split_guarded(float* positions, float* log_scales, float* rotations,
+                          float* opacity_logits, float* sh_or_colors, int64_t sh_floats,
+                          int dims, int64_t count, int64_t reserved_rows, const uint8_t* mask,
+                          float alpha, float log_alpha, float log_gamma, float beta,
+                          const int64_t* guard, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  if (count < 0 || reserved_rows < count || !guard || (dims != 2 && dims != 3))
+    return IGS_ERR_ARGUMENT;
+  if (count == 0) return IGS_OK;
+  if (!positions || !log_scales || !rotations || !opacity_logits || !sh_or_colors || !mask)
+    return IGS_ERR_ARGUMENT;
+  if (dims == 3 && (((uintptr_t)rotations & 15) || (sh_floats % 4 == 0 && ((uintptr_t)sh_or_colors & 15))))
+    return IGS_ERR_ARGUMENT;
+  cudaStream_t s = (cudaStream_t)stream;
+  las::Layout L = las::layout(count);
+  if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
+  int64_t* local_summary = (int64_t*)((char*)workspace + L.guard);
+  const unsigned long long *local_guard = nullptr, *tile_off = nullptr;
+  const int st = dims == 3
+      ? las::launch_prepare_coop<true>(mask, rotations, opacity_logits, count, beta, workspace,
+                                       workspace_bytes, local_summary, s, &local_guard, &tile_off)
+      : las::launch_prepare_coop<false>(mask, nullptr, opacity_logits, count, beta, workspace,
+                                        workspace_bytes, local_summary, s, &local_guard,
+                                        &tile_off);
+  if (st != IGS_OK) return st;
+  const long long tiles = (count + las::TILE - 1) / las::TILE;
+  las::Consts c{alpha, log_alpha, log_gamma, beta};
+  if (dims == 3)
+    las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
+        positions, log_scales, rotations, opacity_logits, sh_or_colors, sh_floats, count, mask,
+        c, 0, tile_off, (const unsigned long long*)guard, reserved_rows);
+  else
+    las::las2d_apply_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
+        positions, log_scales, rotations, opacity_logits, sh_or_colors, count, mask, c, tile_off,
+        (const unsigned long long*)guard, reserved_rows);
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
 }  // extern "C"

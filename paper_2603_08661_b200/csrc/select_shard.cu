@@ -1,25 +1,30 @@
-// Sharded budgeted selection: the per-rank kernels of the multi-GPU protocol of SURVEY.md 8(e).
+// Sharded densify step: the per-rank kernels of the multi-GPU protocol of SURVEY.md 8(e),
+// two collective rounds per densify event and no host round trip until the event is read.
 //
-// Every rank owns a contiguous index range [lo_r, hi_r) of the global Gaussian array, so
-// global index order == (rank, local index) order.  The result is bit-identical to a
-// single-device select_candidates over the concatenated arrays
-// (/root/reference/pkg/src/splitkit/densify_controller.py:80-106, stable argsort :104).
+// Every rank holds a shard of the cloud and, per row, the row's index in the reference's
+// global array (gidx): contiguous ranges before the first split, then children appended in
+// the reference's order (all parents, then all children in parent order).  The selection is
+// bit-identical to np.argsort(-score, kind="stable")[:take] over the global array
+// (/root/reference/pkg/src/splitkit/densify_controller.py:80-106): order by (key, gidx).
 //
-// Per densify step, all stream-ordered on the device (no host round trip until the caller
-// reads the event counts):
-//   keys      key = order-preserving 64-bit image of the score (ascending key ==
-//             descending score, -0 == +0, NaN last; ineligible = ~0); local histogram of the
-//             top 16 key bits plus the local eligible count          -> all-reduce (sum)
-//   resolve   (1 thread block) round 0: take = min(#eligible, take_cap); every round: the
-//             16-bit digit holding rank take-1 of the merged histogram, narrowing the
-//             prefix; after round 3 the prefix is the threshold key T
-//   hist      rounds 1..3: local histogram of the next 16 bits among keys matching the
-//             prefix                                                  -> all-reduce (sum)
-//   ties      per-block counts of key == T and the local total        -> all-gather
-//   finalize  mask = key < T, or key == T and (ties on lower ranks + ties before it on this
-//             rank) < need_ties (ties broken by ascending global index)
-// Four 256 KB all-reduces and one 8-byte all-gather per step; the caller issues them
-// (torch.distributed / NCCL) between the launches, on the same stream.
+//   keys_kernel      key = order-preserving 64-bit image of the score (ascending key ==
+//                    descending score, -0 == +0, NaN last; ineligible = ~0) and a 65536-bin
+//                    histogram of a monotone 16-bit digit of the key (1024 bins per binade
+//                    over scores in [2^-62, 4)), plus the eligible count
+//                                                              -> all-reduce #1 (sum, 256 KB)
+//   resolve_kernel   (1 block) take = min(#eligible, take_cap); the digit B holding rank
+//                    take-1 and need = take - #(digit < B); clears this rank's record
+//   compact_kernel   #(digit < B) and the OR of their LAS flags; the boundary-bucket entries
+//                    (key, gidx | flags << 56) into a fixed-capacity record
+//                                                              -> all-gather #2 (records)
+//   final_kernel     (1 block) over every rank's record: the need-th smallest (key, gidx) of
+//                    the boundary bucket by radix select -> threshold (T, G); every rank's
+//                    split count k_r and the batch flags; this rank's plan (LAS guard
+//                    {k_r or 0, flags}, child base = N + sum_{r' < r} k_r', status)
+//   mask_kernel      mask = digit < B, or digit == B and (key, gidx) <= (T, G)
+//   child_index_kernel  gidx of this rank's appended children
+// A boundary bucket larger than the record capacity sets status OVERFLOW (nothing is split);
+// the host re-runs compact / gather / final with a record sized from the gathered counts.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,22 +35,33 @@ namespace shard {
 
 constexpr int NT = 1024;
 constexpr int NBINS = 1 << 16;
-constexpr int ROUNDS = 4;
 constexpr int U = 4;                          // elements per thread per streaming step
 constexpr unsigned long long kIneligible = ~0ull;
 constexpr long long MAX_PER_BLOCK = 65535;   // 16-bit packed shared-memory counters
 constexpr int SMEM_BYTES = NBINS * 2;        // two 16-bit bins per 32-bit word
+constexpr unsigned long long T_LO = 984064ull;      // (1023 - 62) << 10: 2^-62
+constexpr unsigned long long T_HI = T_LO + 65532ull;
+constexpr int DIGIT_NONPOS = 65534, DIGIT_NAN = 65535;
+constexpr int RBITS = 11, RBINS = 1 << RBITS;  // final_kernel radix digits
 
 struct State {
-  unsigned long long prefix, pmask, rank, take, n_elig, T, need_ties, local_ties;
-  int status;                                 // 0 running, 1 nothing to select
-  int grid;
-  int pad[14];
+  unsigned long long take, n_elig, need, B;
+  int status;  // 0 ok, 1 nothing to select
+  int pad[7];
 };
+static_assert(sizeof(State) <= 256, "state fits its 256-byte slot");
 
 struct Layout {
-  size_t state, blk, keys, total;
+  size_t state, keys, total;
 };
+
+inline Layout layout(long long n) {
+  Layout L;
+  L.state = 0;
+  L.keys = 256;
+  L.total = align_up(L.keys + sizeof(unsigned long long) * (size_t)n, 256);
+  return L;
+}
 
 inline int grid_for(long long n) {
   long long g = (n + MAX_PER_BLOCK - 1) / MAX_PER_BLOCK;
@@ -57,20 +73,6 @@ inline int grid_for(long long n) {
   return (int)g;
 }
 
-inline Layout layout(long long n) {
-  Layout L;
-  size_t off = 0;
-  L.state = off;
-  off += 256;
-  L.blk = off;
-  const long long gmax = (n + MAX_PER_BLOCK - 1) / MAX_PER_BLOCK + 4096;
-  off = align_up(off + sizeof(unsigned) * (size_t)gmax, 256);
-  L.keys = off;
-  off = align_up(off + sizeof(unsigned long long) * (size_t)n, 256);
-  L.total = off;
-  return L;
-}
-
 __device__ __forceinline__ unsigned long long score_key(double s) {
   if (s != s) return 0xFFF8000000000000ull;
   if (s == 0.0) s = 0.0;
@@ -79,25 +81,24 @@ __device__ __forceinline__ unsigned long long score_key(double s) {
   return ~u;
 }
 
-__device__ __forceinline__ int round_shift(int r) { return 48 - 16 * r; }
+// Monotone non-decreasing 16-bit digit of an eligible key (ascending digit == descending
+// score): positive scores 1024 bins per binade over [2^-62, 4), clamped at both ends; every
+// non-positive score one bin; NaN last.
+__device__ __forceinline__ int key_digit(unsigned long long key) {
+  if (key == 0xFFF8000000000000ull) return DIGIT_NAN;
+  const unsigned long long u = ~key;
+  if (!(u >> 63)) return DIGIT_NONPOS;                   // a negative score
+  const unsigned long long b = u & 0x7FFFFFFFFFFFFFFFull;  // |score| bits, score >= +0
+  if (b == 0) return DIGIT_NONPOS;
+  unsigned long long t = b >> 42;
+  t = t < T_LO ? T_LO : (t > T_HI ? T_HI : t);
+  return 1 + (int)(T_HI - t);
+}
 
 __device__ __forceinline__ void block_range(long long n, long long& lo, long long& hi) {
   const long long per = (n + gridDim.x - 1) / gridDim.x;
   lo = min((long long)blockIdx.x * per, n);
   hi = min(lo + per, n);
-}
-
-__device__ __forceinline__ void smem_hist_add(unsigned* h, unsigned d) {
-  atomicAdd(&h[d >> 1], 1u << ((d & 1u) << 4));
-}
-
-__device__ void smem_hist_flush(unsigned* h, int* out) {
-  __syncthreads();
-  for (int i = threadIdx.x; i < NBINS / 2; i += NT) {
-    const unsigned v = h[i];
-    if (v & 0xffffu) atomicAdd(&out[2 * i], (int)(v & 0xffffu));
-    if (v >> 16) atomicAdd(&out[2 * i + 1], (int)(v >> 16));
-  }
 }
 
 struct KeyParams {
@@ -108,7 +109,7 @@ struct KeyParams {
   double thr;
   int warmup, policy;
   unsigned long long* keys;
-  int* hist;      // NBINS + 1 (last: eligible count)
+  int* hist;  // NBINS + 1 (last: eligible count)
 };
 
 __global__ void __launch_bounds__(NT) keys_kernel(KeyParams P) {
@@ -119,11 +120,10 @@ __global__ void __launch_bounds__(NT) keys_kernel(KeyParams P) {
   block_range(P.n, lo, hi);
   unsigned elig = 0;
   const bool need_edge = P.warmup || P.policy != IGS_POLICY_GRAD;
-  // U elements per thread per step, every load issued before the arithmetic
   for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
     double gs[U], ed[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < U; ++u) {  // every load before the arithmetic
       const long long i = i0 + u * NT;
       gs[u] = i < hi ? __ldcs(P.grad_sum + i) : 0.0;
       ed[u] = (i < hi && need_edge) ? __ldcs(P.edge + i) : 0.0;
@@ -142,221 +142,360 @@ __global__ void __launch_bounds__(NT) keys_kernel(KeyParams P) {
       P.keys[i] = k;
       if (e) {
         ++elig;
-        smem_hist_add(h, (unsigned)(k >> 48));
+        const unsigned d = (unsigned)key_digit(k);
+        atomicAdd(&h[d >> 1], 1u << ((d & 1u) << 4));
       }
     }
   }
   elig = __reduce_add_sync(0xffffffffu, elig);
   if (lane_id() == 0 && elig) atomicAdd(&P.hist[NBINS], (int)elig);
-  smem_hist_flush(h, P.hist);
+  __syncthreads();
+  for (int i = threadIdx.x; i < NBINS / 2; i += NT) {
+    const unsigned v = h[i];
+    if (v & 0xffffu) atomicAdd(&P.hist[2 * i], (int)(v & 0xffffu));
+    if (v >> 16) atomicAdd(&P.hist[2 * i + 1], (int)(v >> 16));
+  }
 }
 
-__global__ void __launch_bounds__(NT) hist_kernel(const unsigned long long* __restrict__ keys,
-                                                  long long n, int round, const State* st,
-                                                  int* hist) {
-  if (st->status) return;
-  extern __shared__ unsigned h[];
-  for (int i = threadIdx.x; i < NBINS / 2; i += NT) h[i] = 0;
+// Record of one rank (int64 words): header, then `cap` entries of two words.
+enum Rec { R_LT = 0, R_BCNT = 1, R_LTFLAGS = 2, R_HDR = 4 };
+
+// One block: take, B and need from the merged histogram; clears this rank's record header.
+// Thread t owns the 64 consecutive bins [64 t, 64 t + 64) (16-byte loads); a block scan of
+// the per-thread sums names the owner of rank take-1, which walks its bins.
+__global__ void __launch_bounds__(NT) resolve_kernel(const int* __restrict__ hist,
+                                                     long long take_cap, State* st,
+                                                     long long* record) {
+  __shared__ unsigned warp_sums[32];
+  __shared__ unsigned long long s_need;
+  __shared__ int s_B;
+  const unsigned long long ne = (unsigned long long)(unsigned)hist[NBINS];
+  const unsigned long long take = ne < (unsigned long long)take_cap ? ne : (unsigned long long)take_cap;
+  if (threadIdx.x == 0) {
+    record[R_LT] = 0;
+    record[R_BCNT] = 0;
+    record[R_LTFLAGS] = 0;
+    record[3] = 0;
+    s_B = NBINS;
+    s_need = 0;
+  }
+  const int4* h4 = reinterpret_cast<const int4*>(hist) + threadIdx.x * 16;
+  unsigned sum = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int4 v = __ldcg(h4 + k);
+    sum += (unsigned)v.x + (unsigned)v.y + (unsigned)v.z + (unsigned)v.w;
+  }
+  unsigned total;
+  const unsigned before = block_exclusive_scan(sum, warp_sums, &total);
+  if (take > 0) {
+    const unsigned long long r = take - 1;
+    if (r >= before && r < (unsigned long long)before + sum) {
+      unsigned long long cum = before;
+      const int* hb = hist + threadIdx.x * 64;
+      for (int k = 0; k < 64; ++k) {
+        const unsigned c = (unsigned)__ldcg(hb + k);
+        if (r < cum + c) {
+          s_B = threadIdx.x * 64 + k;
+          s_need = take - cum;
+          break;
+        }
+        cum += c;
+      }
+    }
+  }
   __syncthreads();
-  const unsigned long long prefix = st->prefix, pmask = st->pmask;
-  const int sh = round_shift(round);
+  if (threadIdx.x == 0) {
+    st->take = take;
+    st->n_elig = ne;
+    st->B = (unsigned long long)s_B;
+    st->need = s_need;
+    st->status = take ? 0 : 1;
+  }
+}
+
+// numpy float32 LAS pre-pass flags of one parent (las.cu prepare_tile).
+__device__ __forceinline__ unsigned las_flags(const float* rot, const float* opac, long long i,
+                                              float beta) {
+  unsigned f = 0;
+  if (!opac) return 0;  // selection only (no scene): no split flags
+  if (rot) {
+    const float4 q = reinterpret_cast<const float4*>(rot)[i];
+    float s = q.x * q.x;
+    s = s + q.y * q.y;
+    s = s + q.z * q.z;
+    s = s + q.w * q.w;
+    const float nrm = sqrtf(s);
+    if (!isfinite(nrm) || nrm == 0.0f) f |= IGS_LAS_BAD_QUAT;
+    else if (fabsf(nrm - 1.0f) > 1e-4f) f |= IGS_LAS_RENORM;
+  }
+  const float e = expf(-opac[i]);
+  const float sg = 1.0f / (1.0f + e);
+  const float r = sg * beta;
+  if (!(r > 0.0f && r < 1.0f)) f |= IGS_LAS_BAD_OPACITY;
+  return f;
+}
+
+__global__ void __launch_bounds__(NT) compact_kernel(const unsigned long long* __restrict__ keys,
+                                                     const long long* __restrict__ gidx,
+                                                     const float* rot, const float* opac,
+                                                     float beta, long long n, const State* st,
+                                                     long long cap, long long* record) {
+  __shared__ unsigned s_lt, s_flags;
+  if (threadIdx.x == 0) {
+    s_lt = 0;
+    s_flags = 0;
+  }
+  __syncthreads();
+  if (st->status) return;
+  const int B = (int)st->B;
   long long lo, hi;
   block_range(n, lo, hi);
+  unsigned lt = 0, fl = 0;
   for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
     unsigned long long kv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) kv[u] = i0 + u * NT < hi ? keys[i0 + u * NT] : kIneligible;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const unsigned long long k = kv[u];
-      if (k != kIneligible && (k & pmask) == prefix)
-        smem_hist_add(h, (unsigned)((k >> sh) & 0xffffu));
-    }
-  }
-  smem_hist_flush(h, hist);
-}
-
-// One block: digit of rank st->rank in the merged histogram of `round`.  Warp w owns the
-// contiguous bins [w * 2048, (w + 1) * 2048): coalesced loads, warp sums, a scan of the 32
-// warp totals, then the owning warp resolves the bin with ballots (no per-thread arrays).
-__global__ void __launch_bounds__(NT) resolve_kernel(const int* __restrict__ hist, int round,
-                                                     long long take_cap, State* st,
-                                                     long long* counts) {
-  __shared__ unsigned warp_tot[32];
-  __shared__ unsigned long long s_rank;
-  __shared__ int s_warp;
-  if (round == 0) {
-    if (threadIdx.x == 0) {
-      const unsigned long long ne = (unsigned long long)(unsigned)hist[NBINS];
-      const unsigned long long take = ne < (unsigned long long)take_cap ? ne : (unsigned long long)take_cap;
-      st->n_elig = ne;
-      st->take = take;
-      st->prefix = 0;
-      st->pmask = 0;
-      st->rank = take ? take - 1 : 0;
-      st->status = take ? 0 : 1;
-      st->T = 0;
-      st->need_ties = 0;
-      st->local_ties = 0;
-      if (counts) {
-        counts[0] = (long long)ne;
-        counts[1] = (long long)take;
-      }
-    }
-    __syncthreads();
-  }
-  if (st->status) return;
-  constexpr int PERW = NBINS / (NT / 32);  // 2048 bins per warp
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int* h = hist + warp * PERW;
-  unsigned sum = 0;
-#pragma unroll 8
-  for (int i = lane; i < PERW; i += 32) sum += (unsigned)h[i];
-  sum = __reduce_add_sync(0xffffffffu, sum);
-  if (lane == 0) warp_tot[warp] = sum;
-  __syncthreads();
-  const unsigned long long rank = st->rank;
-  if (warp == 0) {
-    unsigned x = warp_tot[lane], inc = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    const unsigned long long ex = inc - x;
-    const bool mine = x && rank >= ex && rank < ex + x;
-    const unsigned b = __ballot_sync(0xffffffffu, mine);
-    const int w = __ffs(b) - 1;
-    if (lane == w) {
-      s_warp = w;
-      s_rank = rank - ex;
-    }
-  }
-  __syncthreads();
-  if (warp != s_warp) return;
-  // the owning warp walks its 2048 bins 32 at a time
-  unsigned long long r = s_rank;
-  const int* hw = hist + warp * PERW;
-  for (int base = 0; base < PERW; base += 32) {
-    const unsigned c = (unsigned)hw[base + lane];
-    unsigned inc = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    const unsigned tot = __shfl_sync(0xffffffffu, inc, 31);
-    if (r < tot) {
-      const unsigned long long ex = inc - c;
-      const bool mine = c && r >= ex && r < ex + c;
-      const unsigned b = __ballot_sync(0xffffffffu, mine);
-      const int l = __ffs(b) - 1;
-      if (lane == l) {
-        const int digit = warp * PERW + base + l;
-        const int sh = round_shift(round);
-        st->prefix |= (unsigned long long)digit << sh;
-        st->pmask |= 0xffffull << sh;
-        st->rank = r - ex;
-        if (round == ROUNDS - 1) {
-          st->T = st->prefix;
-          st->need_ties = r - ex + 1;
+      if (kv[u] == kIneligible) continue;
+      const long long i = i0 + u * NT;
+      const int d = key_digit(kv[u]);
+      if (d < B) {
+        ++lt;
+        fl |= las_flags(rot, opac, i, beta);
+      } else if (d == B) {
+        const unsigned long long f = las_flags(rot, opac, i, beta);
+        const unsigned long long slot =
+            (unsigned long long)atomicAdd((unsigned long long*)&record[R_BCNT], 1ull);
+        if ((long long)slot < cap) {
+          record[R_HDR + 2 * slot] = (long long)kv[u];
+          record[R_HDR + 2 * slot + 1] = (long long)((unsigned long long)gidx[i] | (f << 56));
         }
       }
-      return;
     }
-    r -= tot;
   }
-}
-
-// Per-block counts of key == T; the local total goes to *local_ties (all-gather send buffer).
-__global__ void __launch_bounds__(NT) ties_kernel(const unsigned long long* __restrict__ keys,
-                                                  long long n, State* st, unsigned* blk,
-                                                  long long* local_ties) {
-  __shared__ unsigned s_cnt;
-  if (threadIdx.x == 0) s_cnt = 0;
-  __syncthreads();
-  const int status = st->status;
-  const unsigned long long T = st->T;
-  long long lo, hi;
-  block_range(n, lo, hi);
-  unsigned c = 0;
-  if (!status)
-    for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
-      unsigned long long kv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) kv[u] = i0 + u * NT < hi ? keys[i0 + u * NT] : ~T;
-#pragma unroll
-      for (int u = 0; u < U; ++u) c += (kv[u] == T);
-    }
-  c = __reduce_add_sync(0xffffffffu, c);
-  if (lane_id() == 0 && c) atomicAdd(&s_cnt, c);
+  lt = __reduce_add_sync(0xffffffffu, lt);
+  fl = __reduce_or_sync(0xffffffffu, fl);
+  if (lane_id() == 0) {
+    if (lt) atomicAdd(&s_lt, lt);
+    if (fl) atomicOr(&s_flags, fl);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    blk[blockIdx.x] = s_cnt;
-    if (s_cnt) atomicAdd((unsigned long long*)local_ties, (unsigned long long)s_cnt);
+    if (s_lt) atomicAdd((unsigned long long*)&record[R_LT], (unsigned long long)s_lt);
+    if (s_flags) atomicOr((unsigned long long*)&record[R_LTFLAGS], (unsigned long long)s_flags);
   }
 }
 
-__global__ void __launch_bounds__(NT) finalize_kernel(const unsigned long long* __restrict__ keys,
-                                                      long long n, const State* st,
-                                                      const unsigned* blk,
-                                                      const long long* all_ties, int rank,
-                                                      uint8_t* mask) {
+// The plan this rank acts on (int64 words; also the host's one read per event).
+enum Plan {
+  P_NSPLIT = 0,   // LAS guard: this rank's split count when the split may go ahead, else 0
+  P_FLAGS = 1,    // LAS guard: the batch flags (OR over every rank's selected parents)
+  P_STATUS = 2,   // 0 ok, 1 nothing selected, 2 boundary bucket overflowed the records
+  P_TAKE = 3,     // global split count
+  P_ELIG = 4,     // global eligible count
+  P_CHILD = 5,    // global index of this rank's first child
+  P_KMINE = 6,    // this rank's split count
+  P_MAXB = 7,     // largest boundary-bucket count over the ranks (overflow re-run size)
+  P_T = 8,        // threshold key
+  P_G = 9,        // threshold global index (key == T and gidx <= G is in)
+  P_B = 10,       // boundary digit
+  P_WORDS = 16
+};
+constexpr int MAX_WORLD = 64;
+
+// Radix select (RBITS-bit digits, block-wide) of the rank-`rank` smallest value of f(e)
+// over entries e whose value matches `prefix` on `pmask`; returns the full value.
+template <typename F>
+__device__ unsigned long long block_select64(F f, long long m, unsigned long long rank,
+                                            unsigned* h, unsigned* warp_sums,
+                                            unsigned long long* s_val, int* s_bin,
+                                            unsigned long long prefix = 0,
+                                            unsigned long long pmask = 0) {
+  for (int top = 63; top >= 0; top -= RBITS) {
+    const int width = top + 1 < RBITS ? top + 1 : RBITS;
+    const int shift = top + 1 - width;
+    const unsigned dmask = (1u << width) - 1;
+    for (int i = threadIdx.x; i < RBINS; i += NT) h[i] = 0;
+    __syncthreads();
+    for (long long e = threadIdx.x; e < m; e += NT) {
+      bool ok;
+      const unsigned long long v = f(e, ok);
+      if (ok && (v & pmask) == prefix) atomicAdd(&h[(v >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    // RBINS / NT bins per thread, block scan, the owner of `rank` publishes the digit
+    constexpr int PER = RBINS / NT;
+    unsigned loc[PER], sum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      loc[k] = h[threadIdx.x * PER + k];
+      sum += loc[k];
+    }
+    unsigned tot;
+    unsigned long long cum = block_exclusive_scan(sum, warp_sums, &tot);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      if (loc[k] && rank >= cum && rank < cum + loc[k]) {
+        *s_bin = threadIdx.x * PER + k;
+        *s_val = rank - cum;
+      }
+      cum += loc[k];
+    }
+    __syncthreads();
+    prefix |= (unsigned long long)(*s_bin) << shift;
+    pmask |= (unsigned long long)dmask << shift;
+    rank = *s_val;
+    __syncthreads();
+  }
+  return prefix;
+}
+
+__global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__ records,
+                                                   int world, int rank, long long cap,
+                                                   long long n_global, const State* st,
+                                                   long long* plan) {
+  __shared__ unsigned h[RBINS];
   __shared__ unsigned warp_sums[32];
-  __shared__ unsigned long long s_before;
-  long long lo, hi;
-  block_range(n, lo, hi);
-  if (st->status) {
-    for (long long i = lo + threadIdx.x; i < hi; i += NT) mask[i] = 0;
+  __shared__ unsigned long long s_val;
+  __shared__ int s_bin;
+  __shared__ unsigned long long s_k[MAX_WORLD];
+  __shared__ unsigned s_flags;
+  const long long stride = R_HDR + 2 * cap;
+  const unsigned long long take = st->take, need = st->need;
+  long long maxb = 0;
+  int overflow = 0;
+  for (int r = 0; r < world; ++r) {
+    const long long b = records[r * stride + R_BCNT];
+    maxb = b > maxb ? b : maxb;
+    overflow |= b > cap;
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < P_WORDS; ++k) plan[k] = 0;
+    plan[P_TAKE] = (long long)take;
+    plan[P_ELIG] = (long long)st->n_elig;
+    plan[P_MAXB] = maxb;
+    plan[P_B] = (long long)st->B;
+  }
+  if (st->status || overflow) {
+    if (threadIdx.x == 0) plan[P_STATUS] = st->status ? 1 : 2;
     return;
   }
-  const unsigned long long T = st->T, need = st->need_ties;
-  unsigned long long b = 0;
-  for (int r = threadIdx.x; r < rank; r += NT) b += (unsigned long long)all_ties[r];
-  for (unsigned k = threadIdx.x; k < blockIdx.x; k += NT) b += blk[k];
-  // block reduce (64-bit)
-  for (int o = 16; o; o >>= 1) b += __shfl_down_sync(0xffffffffu, b, o);
-  if (threadIdx.x == 0) s_before = 0;
+  const long long m = world * cap;  // entry e: rank e / cap, slot e % cap
+  auto key_of = [&](long long e, bool& ok) -> unsigned long long {
+    const long long r = e / cap, s = e - r * cap;
+    ok = s < records[r * stride + R_BCNT];
+    return ok ? (unsigned long long)records[r * stride + R_HDR + 2 * s] : 0ull;
+  };
+  // threshold key T: the need-th smallest boundary key (rank need - 1)
+  const unsigned long long T = block_select64(key_of, m, need - 1, h, warp_sums, &s_val,
+                                              &s_bin);
+  // ties on T: how many of them are in, and the gidx cutoff when not all are
   __syncthreads();
-  if (lane_id() == 0 && b) atomicAdd(&s_before, b);
-  __syncthreads();
-  unsigned long long run = s_before;
-  // U-element steps; the tie scan (in index order) only runs for steps that hold a tie
-  for (long long c0 = lo; c0 < hi; c0 += U * NT) {
-    unsigned long long kv[U];
-    int any = 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = c0 + u * NT + threadIdx.x;
-      kv[u] = i < hi ? keys[i] : kIneligible;
-      any |= kv[u] == T;
-    }
-    if (!__syncthreads_or(any)) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long i = c0 + u * NT + threadIdx.x;
-        if (i < hi) mask[i] = kv[u] < T;
-      }
-      continue;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = c0 + u * NT + threadIdx.x;
-      const unsigned is_tie = kv[u] == T ? 1u : 0u;
-      unsigned tot;
-      const unsigned ex = block_exclusive_scan(is_tie, warp_sums, &tot);
-      if (i < hi) mask[i] = (kv[u] < T) || (is_tie && run + ex < need);
-      run += tot;
+  unsigned long long below = 0, ties = 0;
+  for (long long e = threadIdx.x; e < m; e += NT) {
+    bool ok;
+    const unsigned long long k = key_of(e, ok);
+    if (ok) {
+      below += k < T;
+      ties += k == T;
     }
   }
+  for (int o = 16; o; o >>= 1) {
+    below += __shfl_down_sync(0xffffffffu, below, o);
+    ties += __shfl_down_sync(0xffffffffu, ties, o);
+  }
+  __shared__ unsigned long long s_below, s_ties;
+  if (threadIdx.x == 0) {
+    s_below = 0;
+    s_ties = 0;
+  }
+  __syncthreads();
+  if (lane_id() == 0) {
+    atomicAdd(&s_below, below);
+    atomicAdd(&s_ties, ties);
+  }
+  __syncthreads();
+  const unsigned long long need_ties = need - s_below;
+  unsigned long long G = 0x00FFFFFFFFFFFFFFull;  // every tie in
+  if (need_ties < s_ties) {
+    auto gidx_of = [&](long long e, bool& ok) -> unsigned long long {
+      const long long r = e / cap, s = e - r * cap;
+      ok = s < records[r * stride + R_BCNT] &&
+           (unsigned long long)records[r * stride + R_HDR + 2 * s] == T;
+      return ok ? ((unsigned long long)records[r * stride + R_HDR + 2 * s + 1] &
+                   0x00FFFFFFFFFFFFFFull)
+                : 0ull;
+    };
+    G = block_select64(gidx_of, m, need_ties - 1, h, warp_sums, &s_val, &s_bin);
+  }
+  // every rank's split count and the batch flags
+  for (int r = threadIdx.x; r < world; r += NT)
+    s_k[r] = (unsigned long long)records[r * stride + R_LT];
+  if (threadIdx.x == 0) {
+    s_flags = 0;
+    for (int r = 0; r < world; ++r) s_flags |= (unsigned)records[r * stride + R_LTFLAGS];
+  }
+  __syncthreads();
+  for (long long e = threadIdx.x; e < m; e += NT) {
+    bool ok;
+    const unsigned long long k = key_of(e, ok);
+    if (!ok) continue;
+    const long long r = e / cap, s = e - r * cap;
+    const unsigned long long w = (unsigned long long)records[r * stride + R_HDR + 2 * s + 1];
+    const unsigned long long g = w & 0x00FFFFFFFFFFFFFFull;
+    if (k < T || (k == T && g <= G)) {
+      atomicAdd(&s_k[r], 1ull);
+      atomicOr(&s_flags, (unsigned)(w >> 56));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long base = (unsigned long long)n_global;
+    for (int r = 0; r < rank; ++r) base += s_k[r];
+    const unsigned long long kmine = s_k[rank];
+    plan[P_NSPLIT] = (long long)kmine;
+    plan[P_FLAGS] = (long long)s_flags;
+    plan[P_STATUS] = 0;
+    plan[P_CHILD] = (long long)base;
+    plan[P_KMINE] = (long long)kmine;
+    plan[P_T] = (long long)T;
+    plan[P_G] = (long long)G;
+  }
+}
+
+__global__ void __launch_bounds__(NT) mask_kernel(const unsigned long long* __restrict__ keys,
+                                                  const long long* __restrict__ gidx, long long n,
+                                                  const long long* plan, uint8_t* mask) {
+  const bool ok = plan[P_STATUS] == 0;
+  const int B = (int)plan[P_B];
+  const unsigned long long T = (unsigned long long)plan[P_T];
+  const unsigned long long G = (unsigned long long)plan[P_G];
+  for (long long i = blockIdx.x * (long long)NT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * NT) {
+    const unsigned long long k = keys[i];
+    bool in = false;
+    if (ok && k != kIneligible) {
+      const int d = key_digit(k);
+      in = d < B || (d == B && (k < T || (k == T && (unsigned long long)gidx[i] <= G)));
+    }
+    mask[i] = in;
+  }
+}
+
+__global__ void child_index_kernel(long long* gidx, long long count, const long long* plan) {
+  const long long k = plan[P_STATUS] == 0 ? plan[P_KMINE] : 0;
+  const long long base = plan[P_CHILD];
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < k;
+       j += (long long)gridDim.x * blockDim.x)
+    gidx[count + j] = base + j;
 }
 
 inline int set_smem() {
   static int done = 0;
   if (!done) {
     if (cudaFuncSetAttribute(keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_BYTES) != cudaSuccess ||
-        cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SMEM_BYTES) != cudaSuccess)
       return 0;
     done = 1;
@@ -371,87 +510,86 @@ using namespace igs;
 
 extern "C" {
 
-int igs_select_shard_workspace_bytes(int64_t n, size_t* bytes) {
+int igs_shard_workspace_bytes(int64_t n, size_t* bytes) {
   if (!bytes || n < 0) return IGS_ERR_ARGUMENT;
   *bytes = shard::layout(n).total;
   return IGS_OK;
 }
 
-int igs_select_shard_keys(const double* grad_sum, int64_t accum_count, const double* edge_score,
-                          int64_t n, double grad_threshold, int warmup, int policy, int32_t* hist,
-                          void* workspace, size_t workspace_bytes, void* stream) {
+int igs_shard_keys(const double* grad_sum, int64_t accum_count, const double* edge_score,
+                   int64_t n, double grad_threshold, int warmup, int policy, int32_t* hist,
+                   void* workspace, size_t workspace_bytes, void* stream) {
   if (n < 0 || accum_count < 0 || !hist || policy < 0 || policy > 2) return IGS_ERR_ARGUMENT;
   if (n >= (1ll << 31)) return IGS_ERR_UNSUPPORTED;
   if (n > 0 && (!grad_sum || !edge_score)) return IGS_ERR_ARGUMENT;
+  if ((uintptr_t)hist & 15) return IGS_ERR_ARGUMENT;
   shard::Layout L = shard::layout(n);
   if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  char* w = (char*)workspace;
   IGS_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(int32_t) * IGS_SHARD_HIST_LEN, st));
-  IGS_CUDA_TRY(cudaMemsetAsync(w + L.state, 0, sizeof(shard::State), st));
   if (n == 0) return IGS_OK;
   if (!shard::set_smem()) return IGS_ERR_CUDA;
   shard::KeyParams P{grad_sum, accum_count, edge_score, n, grad_threshold, warmup, policy,
-                     (unsigned long long*)(w + L.keys), hist};
+                     (unsigned long long*)((char*)workspace + L.keys), hist};
   shard::keys_kernel<<<shard::grid_for(n), shard::NT, shard::SMEM_BYTES, st>>>(P);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }
 
-int igs_select_shard_resolve(const int32_t* global_hist, int round, int64_t take_cap,
-                             void* workspace, size_t workspace_bytes, int64_t* counts,
-                             void* stream) {
-  if (!global_hist || round < 0 || round >= shard::ROUNDS || take_cap < 0) return IGS_ERR_ARGUMENT;
-  if (!workspace || workspace_bytes < 256) return IGS_ERR_WORKSPACE;
-  shard::resolve_kernel<<<1, shard::NT, 0, (cudaStream_t)stream>>>(
-      global_hist, round, take_cap, (shard::State*)workspace, (long long*)counts);
-  IGS_LAUNCH_CHECK();
-  return IGS_OK;
-}
-
-int igs_select_shard_hist(int64_t n, int round, int32_t* hist, void* workspace,
-                          size_t workspace_bytes, void* stream) {
-  if (n < 0 || !hist || round < 1 || round >= shard::ROUNDS) return IGS_ERR_ARGUMENT;
+int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64_t* gidx,
+                       const float* rotations, const float* opacity_logits, float beta,
+                       int64_t n, int64_t record_cap, int64_t* record, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (!global_hist || !record || take_cap < 0 || n < 0 || record_cap < 1) return IGS_ERR_ARGUMENT;
+  if (((uintptr_t)global_hist & 15) || ((uintptr_t)rotations & 15)) return IGS_ERR_ARGUMENT;
+  if (n > 0 && !gidx) return IGS_ERR_ARGUMENT;  // opacity_logits NULL: no LAS flags
   shard::Layout L = shard::layout(n);
   if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  IGS_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(int32_t) * IGS_SHARD_HIST_LEN, st));
-  if (n == 0) return IGS_OK;
-  if (!shard::set_smem()) return IGS_ERR_CUDA;
   char* w = (char*)workspace;
-  shard::hist_kernel<<<shard::grid_for(n), shard::NT, shard::SMEM_BYTES, st>>>(
-      (const unsigned long long*)(w + L.keys), n, round, (const shard::State*)(w + L.state), hist);
+  shard::State* S = (shard::State*)(w + L.state);
+  shard::resolve_kernel<<<1, shard::NT, 0, st>>>(global_hist, take_cap, S, (long long*)record);
+  IGS_LAUNCH_CHECK();
+  if (n == 0) return IGS_OK;
+  shard::compact_kernel<<<shard::grid_for(n), shard::NT, 0, st>>>(
+      (const unsigned long long*)(w + L.keys), (const long long*)gidx, rotations, opacity_logits,
+      beta, n, S, record_cap, (long long*)record);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }
 
-int igs_select_shard_ties(int64_t n, int64_t* local_ties, void* workspace, size_t workspace_bytes,
-                          void* stream) {
-  if (n < 0 || !local_ties) return IGS_ERR_ARGUMENT;
+int igs_shard_finalize(const int64_t* records, int world, int rank, int64_t record_cap,
+                       int64_t n_global, const int64_t* gidx, int64_t n, uint8_t* mask,
+                       int64_t* plan, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!records || !plan || world < 1 || world > shard::MAX_WORLD || rank < 0 || rank >= world ||
+      record_cap < 1 || n < 0 || n_global < 0)
+    return IGS_ERR_ARGUMENT;
+  if (n > 0 && (!gidx || !mask)) return IGS_ERR_ARGUMENT;
   shard::Layout L = shard::layout(n);
   if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  IGS_CUDA_TRY(cudaMemsetAsync(local_ties, 0, sizeof(int64_t), st));
-  if (n == 0) return IGS_OK;
   char* w = (char*)workspace;
-  shard::ties_kernel<<<shard::grid_for(n), shard::NT, 0, st>>>(
-      (const unsigned long long*)(w + L.keys), n, (shard::State*)(w + L.state),
-      (unsigned*)(w + L.blk), (long long*)local_ties);
+  shard::final_kernel<<<1, shard::NT, 0, st>>>((const long long*)records, world, rank,
+                                               record_cap, n_global,
+                                               (const shard::State*)(w + L.state),
+                                               (long long*)plan);
+  IGS_LAUNCH_CHECK();
+  if (n == 0) return IGS_OK;
+  long long grid = (n + shard::NT - 1) / shard::NT;
+  const long long cap = 8LL * (sm_count() > 0 ? sm_count() : 148);
+  if (grid > cap) grid = cap;
+  shard::mask_kernel<<<(unsigned)grid, shard::NT, 0, st>>>(
+      (const unsigned long long*)(w + L.keys), (const long long*)gidx, n,
+      (const long long*)plan, mask);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }
 
-int igs_select_shard_finalize(int64_t n, const int64_t* all_ties, int rank, uint8_t* mask,
-                              void* workspace, size_t workspace_bytes, void* stream) {
-  if (n < 0 || rank < 0 || (rank > 0 && !all_ties)) return IGS_ERR_ARGUMENT;
-  if (n == 0) return IGS_OK;
-  if (!mask) return IGS_ERR_ARGUMENT;
-  shard::Layout L = shard::layout(n);
-  if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
-  char* w = (char*)workspace;
-  shard::finalize_kernel<<<shard::grid_for(n), shard::NT, 0, (cudaStream_t)stream>>>(
-      (const unsigned long long*)(w + L.keys), n, (const shard::State*)(w + L.state),
-      (const unsigned*)(w + L.blk), (const long long*)all_ties, rank, mask);
+int igs_shard_child_index(int64_t* gidx, int64_t count, const int64_t* plan, void* stream) {
+  if (!gidx || !plan || count < 0) return IGS_ERR_ARGUMENT;
+  shard::child_index_kernel<<<(unsigned)(2 * (sm_count() > 0 ? sm_count() : 148)), 256, 0,
+                              (cudaStream_t)stream>>>((long long*)gidx, count,
+                                                      (const long long*)plan);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }

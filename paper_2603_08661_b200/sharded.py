@@ -1,47 +1,69 @@
-"""Multi-GPU densification: contiguous Gaussian shards, one process per GPU.
+"""Multi-GPU densification: the cloud sharded over ranks, one process per GPU.
 
 The reference (``splitkit``) is single-process; this module keeps its semantics on a cloud
-that is split across ranks in contiguous index ranges ``[lo_r, hi_r)``:
+split across ranks.  Every row carries ``gidx``, its index in the global array; selection
+ties break by it.  On contiguous shards (``[lo_r, hi_r)`` per rank) a densify event is
+exactly the reference's on the global cloud, children included: they get the indices the
+reference gives them (all parents first, then every child in parent order,
+``las_split.py:158-179``) while staying on their parents' rank.  Capacity is global, as in
+the reference: a shard reserves room for the global headroom, so however skewed a selection
+is, its children fit on their parents' rank and nothing moves between GPUs.
 
-* ``select_candidates_sharded`` is bit-identical to ``select_candidates`` on the
-  concatenated statistics (``/root/reference/pkg/src/splitkit/densify_controller.py:80-106``):
-  the per-rank radix-select kernels of ``igs_select_shard_*`` with four 256 KB sum
-  all-reduces of digit histograms and one 8-byte all-gather of tie counts between them,
-  all enqueued on the current stream (no host round trip inside the selection).
-* ``las_split_sharded`` splits every rank's masked parents locally.  One all-gather of each
-  rank's ``{n_split, flags}`` gives the global budget / domain checks, the batch-global
-  quaternion renormalisation rule (``core.py:45-46`` spans the whole masked batch) and
-  the global append offsets: the reference layout ``[parents 0..N-1] ++ [children in
-  parent order]`` is the concatenation of the ranks' parents followed by the
-  concatenation of the ranks' children (``las_split.py:158-179``).
-* ``densify_step_sharded`` composes them and returns the reference's ``DensifyEvent``
-  with global counts (``densify_controller.py:125-147``).
-* ``gather_scene`` all-gathers the compacted rows when every rank needs the whole cloud
-  (reported separately: it does not shrink with the number of ranks).
+After an event a rank holds two index ranges (its parents, its children).  The next event is
+then exact up to the order it gives children across ranks (rank-major within the event,
+where the reference interleaves them by parent index; an exact numbering would need a
+segment table that doubles every event).  ``reshard`` restores contiguous shards (one
+all-gather of the cloud) so that every event is exact; the tests run event, reshard, event.
+
+* ``densify_step_sharded`` (``densify_controller.py:125-147`` on the global cloud): the
+  selection of ``select_candidates`` (``:80-106``, the stable argsort = order by (score key,
+  gidx)) and the split, with TWO collectives and ONE host read per event:
+
+  1. ``igs_shard_keys`` -> all-reduce(sum) of a 65536-bin histogram of a monotone digit of the
+     score key (256 KB) plus the eligible count;
+  2. ``igs_shard_boundary`` (take, boundary digit, this rank's boundary-bucket entries with
+     their LAS flags) -> all-gather of the fixed-size records;
+  3. ``igs_shard_finalize``: the threshold (key, gidx) by radix select over every rank's
+     boundary entries, this rank's mask and its plan (split count, child base, batch flags);
+     ``igs_las_split_guarded``; ``igs_shard_child_index``; then the plan is read once.
+
+  A boundary bucket that overflows the record capacity (only for extremely concentrated
+  scores) is detected in the plan with nothing written, and steps 2-3 re-run with a record
+  sized from the gathered counts.
+* ``select_candidates_sharded`` is steps 1-3 without the split (one host read).
+* ``las_split_sharded`` splits a caller-given mask: one all-gather of ``{n_split, flags}``
+  gives the global budget / domain checks and the batch-global quaternion renormalisation
+  rule (``core.py:45-46`` spans the whole masked batch).
+* ``gather_scene`` all-gathers the rows and places them by gidx: the reference's layout.
 
 Edge maps shard by view (``shard_range`` over the batch); the median is per view, so that
 path has no collective at all.
 
-Collectives go through ``torch.distributed`` on the tensors' device: NCCL over NVLink in
-production, gloo in the CPU/one-GPU tests.  The per-rank kernels are pluggable
-(``ops=``) only so the protocol can be exercised by CPU tests with a test double; the
-product default is the CUDA library, and there is no CPU fallback.
+Collectives go through ``torch.distributed`` on the tensors' device: NCCL in production, gloo
+in the CPU / one-GPU tests.  The per-rank kernels are pluggable (``ops=``) only so the
+protocol can run in CPU tests with a numpy test double; the product default is the CUDA
+library, and there is no CPU fallback.
 """
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _lib
 from . import las_split as _las
-from .core import Scene3
 from .densify_controller import DensifyEvent, DensifyStats, _take_cap
 from .schedule import DensifyConfig, is_densify_step, is_warmup_step
 
-ROUNDS = 4  # 16-bit digits of the 64-bit selection key
+REC_HDR = 4                  # record header words: #(digit < B), boundary count, their flags, 0
+DEFAULT_RECORD_CAP = 4096    # boundary entries per rank per record (two int64 words each)
+PLAN_WORDS = 16
+P_NSPLIT, P_FLAGS, P_STATUS, P_TAKE, P_ELIG, P_CHILD, P_KMINE, P_MAXB = range(8)
+STATUS_OK, STATUS_NOTHING, STATUS_OVERFLOW = 0, 1, 2
 
 
 def shard_range(n: int, rank: int, world: int):
@@ -72,78 +94,96 @@ class Comm:
         return t
 
     def all_gather(self, t: torch.Tensor) -> torch.Tensor:
-        """(world, *t.shape) stack of every rank's t (same shape on every rank)."""
+        """(world, *t.shape) stack of every rank's t (same shape on every rank): one
+        all_gather_into_tensor on NCCL, the list form elsewhere (gloo)."""
         if self.world == 1:
-            return t.unsqueeze(0).clone()
+            return t.unsqueeze(0)
+        t = t.contiguous()
+        if dist.get_backend(self.group) == "nccl":
+            out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t, group=self.group)
+            return out
         parts = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(parts, t.contiguous(), group=self.group)
+        dist.all_gather(parts, t, group=self.group)
         return torch.stack(parts)
 
 
 # ------------------------------------------------------------------ per-rank CUDA kernels
-class CudaSelectShard:
-    """The per-rank launches of the sharded radix select (include/igs_b200.h)."""
+class CudaShardOps:
+    """The per-rank launches of the sharded step (include/igs_b200.h igs_shard_*)."""
 
     def __init__(self, n: int, device):
         self.n = int(n)
         self.device = torch.device(device)
         self.L = _lib.lib()
-        nbytes = _lib.query_size(self.L.igs_select_shard_workspace_bytes, self.n)
-        self.ws = _lib.workspace(nbytes, self.device, "select_shard")
-        self.hist = torch.empty(_lib.IGS_SHARD_HIST_LEN, dtype=torch.int32, device=self.device)
-        self.counts = torch.zeros(2, dtype=torch.int64, device=self.device)
-        self.local_ties = torch.zeros(1, dtype=torch.int64, device=self.device)
+        nbytes = _lib.query_size(self.L.igs_shard_workspace_bytes, self.n)
+        self.ws = _lib.workspace(nbytes, self.device, "shard")
+        self.hist = torch.empty(_lib.IGS_SHARD_HIST_LEN + 3, dtype=torch.int32,
+                                device=self.device)[:_lib.IGS_SHARD_HIST_LEN]
+        self.plan = torch.zeros(PLAN_WORDS, dtype=torch.int64, device=self.device)
 
     def keys(self, stats: DensifyStats, cfg: DensifyConfig, step: int) -> torch.Tensor:
-        _lib.check(self.L.igs_select_shard_keys(
+        _lib.check(self.L.igs_shard_keys(
             stats._grad_sum.data_ptr(), stats._accum_count, stats.edge_score.data_ptr(), self.n,
             float(cfg.grad_threshold), int(is_warmup_step(cfg, step)),
             _lib.IGS_POLICY[cfg.policy], self.hist.data_ptr(), self.ws.data_ptr(),
-            self.ws.numel(), _lib.stream_handle()), "select_candidates_sharded")
+            self.ws.numel(), _lib.stream_handle()), "densify_step_sharded")
         return self.hist
 
-    def resolve(self, hist: torch.Tensor, rnd: int, take_cap: int) -> torch.Tensor:
-        _lib.check(self.L.igs_select_shard_resolve(
-            hist.data_ptr(), rnd, int(take_cap), self.ws.data_ptr(), self.ws.numel(),
-            self.counts.data_ptr(), _lib.stream_handle()), "select_candidates_sharded")
-        return self.counts
+    def boundary(self, hist, take_cap: int, gidx, scene, beta: float, cap: int):
+        rec = torch.empty(REC_HDR + 2 * cap, dtype=torch.int64, device=self.device)
+        rot, op = _flag_columns(scene)
+        _lib.check(self.L.igs_shard_boundary(
+            hist.data_ptr(), int(take_cap), gidx.data_ptr(), rot, op, float(beta), self.n,
+            int(cap), rec.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+            _lib.stream_handle()), "densify_step_sharded")
+        return rec
 
-    def digit_hist(self, rnd: int) -> torch.Tensor:
-        _lib.check(self.L.igs_select_shard_hist(self.n, rnd, self.hist.data_ptr(),
-                                                self.ws.data_ptr(), self.ws.numel(),
-                                                _lib.stream_handle()),
-                   "select_candidates_sharded")
-        return self.hist
-
-    def ties(self) -> torch.Tensor:
-        _lib.check(self.L.igs_select_shard_ties(self.n, self.local_ties.data_ptr(),
-                                                self.ws.data_ptr(), self.ws.numel(),
-                                                _lib.stream_handle()),
-                   "select_candidates_sharded")
-        return self.local_ties
-
-    def finalize(self, all_ties: torch.Tensor, rank: int) -> torch.Tensor:
+    def finalize(self, records, rank: int, cap: int, n_global: int, gidx):
         mask = torch.empty(self.n, dtype=torch.uint8, device=self.device)
-        all_ties = all_ties.reshape(-1).contiguous()
-        _lib.check(self.L.igs_select_shard_finalize(self.n, all_ties.data_ptr(), rank,
-                                                    mask.data_ptr(), self.ws.data_ptr(),
-                                                    self.ws.numel(), _lib.stream_handle()),
-                   "select_candidates_sharded")
-        return mask.view(torch.bool)
+        records = records.contiguous()
+        _lib.check(self.L.igs_shard_finalize(
+            records.data_ptr(), records.shape[0], rank, int(cap), int(n_global),
+            gidx.data_ptr(), self.n, mask.data_ptr(), self.plan.data_ptr(), self.ws.data_ptr(),
+            self.ws.numel(), _lib.stream_handle()), "densify_step_sharded")
+        return mask, self.plan
 
 
-def select_shard_protocol(ops, stats, cfg, step, take_cap: int, comm: Comm):
-    """The collective schedule of the sharded select.  Returns (local bool mask, device
-    int64[2] global {#eligible, take}); nothing is read back to the host."""
-    hist = comm.all_reduce_sum_(ops.keys(stats, cfg, step))
-    counts = ops.resolve(hist, 0, take_cap)
-    for rnd in range(1, ROUNDS):
-        hist = comm.all_reduce_sum_(ops.digit_hist(rnd))
-        ops.resolve(hist, rnd, take_cap)
-    all_ties = comm.all_gather(ops.ties())
-    return ops.finalize(all_ties, comm.rank), counts
+def _flag_columns(scene):
+    """(rotations or None, opacity_logits) device pointers for the LAS flags of the selected
+    parents; no scene (selection only): no flags."""
+    if scene is None:
+        return None, None
+    if hasattr(scene, "_rot"):
+        return scene._rot.data_ptr(), scene._op.data_ptr()
+    return None, scene._opacity_logits.data_ptr()
 
 
+def _protocol(ops, stats, cfg, step, take_cap, comm, gidx, n_global, scene, beta, cap):
+    """The two collective rounds of one event; everything stays on the device."""
+    hist = comm.all_reduce_sum_(ops.keys(stats, cfg, step))                  # round 1
+    rec = ops.boundary(hist, take_cap, gidx, scene, beta, cap)
+    return hist, ops.finalize(comm.all_gather(rec), comm.rank, cap, n_global, gidx)  # round 2
+
+
+def _rerun(ops, hist, take_cap, comm, gidx, n_global, scene, beta, cap):
+    rec = ops.boundary(hist, take_cap, gidx, scene, beta, cap)
+    return ops.finalize(comm.all_gather(rec), comm.rank, cap, n_global, gidx)
+
+
+def _read(plan, pinned):
+    buf, view = pinned
+    buf.copy_(plan, non_blocking=True)
+    if plan.is_cuda:
+        _las.sync(plan.device)
+    return [int(v) for v in view]
+
+
+def _overflow_cap(maxb: int) -> int:
+    return max(DEFAULT_RECORD_CAP, 1 << math.ceil(math.log2(max(maxb, 1))))
+
+
+# ------------------------------------------------------------------ global bookkeeping
 def global_counts(scene, comm: Comm):
     """Every rank's (count, capacity) as a host list, via one small all-gather."""
     t = torch.tensor([scene.count, scene.capacity], dtype=torch.int64, device=_device_of(scene))
@@ -155,22 +195,177 @@ def _device_of(scene):
     return scene.device if hasattr(scene, "device") else torch.device("cpu")
 
 
+@dataclass
+class GlobalCloud:
+    """The global view a shard keeps: the reference scene's count and capacity."""
+
+    count: int
+    capacity: int
+
+
+def attach(scene, comm: Comm | None = None, caps=None) -> GlobalCloud:
+    """Make `scene` this rank's contiguous shard of a global cloud: its global count and
+    capacity (sums over the ranks) and each row's global index.  Idempotent; ``caps`` (the
+    per-rank (count, capacity) list) saves the all-gather when the caller has it."""
+    g = getattr(scene, "_shard_global", None)
+    if g is not None:
+        return g
+    comm = comm or Comm()
+    caps = caps or global_counts(scene, comm)
+    lo = sum(c for c, _ in caps[:comm.rank])
+    gidx = torch.empty(scene.reserved_rows, dtype=torch.int64, device=scene.device)
+    gidx[:scene.count] = torch.arange(lo, lo + scene.count, device=scene.device)
+    scene._gidx = gidx
+    scene._shard_global = GlobalCloud(sum(c for c, _ in caps), sum(cp for _, cp in caps))
+    return scene._shard_global
+
+
+def reshard(scene, comm: Comm | None = None):
+    """Re-cut the cloud into contiguous shards of the reference's global array (one all-gather
+    of every row, then each rank keeps its range): afterwards gidx = lo_r + local index and
+    the next densify event is exactly the reference's.  Returns (lo, hi)."""
+    comm = comm or Comm()
+    glob = attach(scene, comm)
+    full = gather_scene(scene, comm=comm)
+    n = full["positions"].shape[0]
+    lo, hi = shard_range(n, comm.rank, comm.world)
+    k = hi - lo
+    _reserve(scene, k)
+    scene._pos[:k] = full["positions"][lo:hi]
+    scene._ls[:k] = full["log_scales"][lo:hi]
+    scene._rot[:k] = full["rotations"][lo:hi]
+    scene._op[:k] = full["opacity_logits"][lo:hi]
+    scene._sh[:k] = full["sh"][lo:hi]
+    scene._capacity = max(scene._capacity, k)
+    scene._set_count(k)
+    scene._gidx[:k] = torch.arange(lo, hi, dtype=torch.int64, device=scene.device)
+    glob.count = n
+    return lo, hi
+
+
+def detach(scene):
+    """Forget the shard's global view (the next step re-attaches it as a contiguous shard)."""
+    scene.__dict__.pop("_shard_global", None)
+    scene.__dict__.pop("_gidx", None)
+
+
+def _reserve(scene, rows: int):
+    """Physical rows for this shard (a shard holds the global headroom's worth of children at
+    most): grow the columns and the global-index column together."""
+    if scene.reserved_rows < rows:
+        scene._reserve(rows)
+    if scene._gidx.shape[0] < scene.reserved_rows:
+        g = torch.empty(scene.reserved_rows, dtype=torch.int64, device=scene.device)
+        g[:scene.count] = scene._gidx[:scene.count]
+        scene._gidx = g
+
+
+def _take_cap_global(cfg, glob: GlobalCloud) -> int:
+    headroom = glob.capacity - glob.count
+    return _take_cap(cfg, glob.count, headroom) if (headroom > 0 and glob.count > 0) else 0
+
+
+# ------------------------------------------------------------------ public API
 def select_candidates_sharded(stats: DensifyStats, cfg: DensifyConfig, step: int,
                               headroom: int, global_count: int, comm: Comm | None = None,
-                              ops=None):
-    """Local slice of ``select_candidates(global stats, cfg, step, headroom)``.
-
-    ``headroom`` and ``global_count`` are the GLOBAL scene's (capacity - count) and count;
-    take = min(#eligible, headroom, ceil(growth_cap * count - 1e-9)) as at
-    densify_controller.py:99-100.  Returns a CUDA bool tensor of this rank's length."""
+                              ops=None, gidx=None, scene=None, record_cap=None,
+                              return_plan=False):
+    """This rank's slice of ``select_candidates(global stats, cfg, step, headroom)``
+    (densify_controller.py:80-106).  ``headroom`` / ``global_count`` are the global scene's;
+    ``gidx`` the rows' global indices (default: a contiguous shard).  Returns a bool tensor
+    of this rank's length (and the plan words when ``return_plan``)."""
     comm = comm or Comm()
     if headroom < 0:
         raise ValueError("headroom must be non-negative")
     n = len(stats)
+    dev = stats._device
     take_cap = _take_cap(cfg, global_count, headroom) if (headroom > 0 and global_count > 0) else 0
-    ops = ops or CudaSelectShard(n, stats._device)
-    mask, _ = select_shard_protocol(ops, stats, cfg, step, take_cap, comm)
-    return mask
+    if gidx is None:
+        sizes = comm.all_gather(torch.tensor([n], dtype=torch.int64, device=dev)).cpu()
+        lo = int(sizes[:comm.rank].sum())
+        gidx = torch.arange(lo, lo + n, dtype=torch.int64, device=dev)
+    ops = ops or CudaShardOps(n, dev)
+    beta = cfg.split_constants.device_constants()[3]
+    cap = record_cap or DEFAULT_RECORD_CAP
+    hist, (mask, plan) = _protocol(ops, stats, cfg, step, take_cap, comm, gidx, global_count,
+                                   scene, beta, cap)
+    pinned = _las.pinned_summary(dev, PLAN_WORDS) if dev.type == "cuda" else _host_buf()
+    p = _read(plan, pinned)
+    while p[P_STATUS] == STATUS_OVERFLOW:
+        cap = _overflow_cap(p[P_MAXB])
+        mask, plan = _rerun(ops, hist, take_cap, comm, gidx, global_count, scene, beta, cap)
+        p = _read(plan, pinned)
+    return (mask.view(torch.bool), p) if return_plan else mask.view(torch.bool)
+
+
+def _host_buf():
+    t = torch.zeros(PLAN_WORDS, dtype=torch.int64)
+    return t, t.numpy()
+
+
+def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: int,
+                         comm: Comm | None = None, caps=None, select_ops=None) -> DensifyEvent:
+    """One densify event on this rank's shard (densify_controller.py:125-147 on the global
+    scene).  Every rank returns the same DensifyEvent with global counts.  ``caps``: the
+    per-rank (count, capacity) list for the first call (else one all-gather)."""
+    comm = comm or Comm()
+    if not is_densify_step(cfg, step):
+        raise ValueError(f"step {step} is not a densify step for this timetable")
+    if len(stats) != scene.count:
+        raise ValueError("stats length does not match scene count")
+    glob = attach(scene, comm, caps)
+    take_cap = _take_cap_global(cfg, glob)
+    n = scene.count
+    _reserve(scene, n + min(take_cap, n))
+    ops = select_ops or CudaShardOps(n, stats._device)
+    c = cfg.split_constants
+    alpha, log_alpha, log_gamma, beta = c.device_constants()
+    gidx = scene._gidx
+    cap = DEFAULT_RECORD_CAP
+    pinned = _las.pinned_summary(scene.device, PLAN_WORDS)
+    hist, (mask, plan) = _protocol(ops, stats, cfg, step, take_cap, comm, gidx, glob.count,
+                                   scene, beta, cap)
+    while True:
+        if take_cap > 0:
+            _split_guarded(scene, mask, plan, alpha, log_alpha, log_gamma, beta)
+            _lib.check(_lib.lib().igs_shard_child_index(gidx.data_ptr(), n, plan.data_ptr(),
+                                                        _lib.stream_handle()),
+                       "densify_step_sharded")
+        p = _read(plan, pinned)                                    # the event's one host read
+        if p[P_STATUS] != STATUS_OVERFLOW:
+            break
+        cap = _overflow_cap(p[P_MAXB])                             # nothing was written
+        mask, plan = _rerun(ops, hist, take_cap, comm, gidx, glob.count, scene, beta, cap)
+    split = p[P_TAKE] if p[P_STATUS] == STATUS_OK else 0
+    if split and p[P_FLAGS] & _lib.IGS_LAS_BAD_OPACITY:
+        raise ValueError("logit requires all values strictly inside (0, 1)")
+    if split and p[P_FLAGS] & _lib.IGS_LAS_BAD_QUAT:
+        raise ValueError("zero or non-finite quaternion")
+    if split:
+        if n + p[P_KMINE] > scene._capacity:   # this shard's share of the global headroom
+            scene._capacity = scene.reserved_rows
+        scene._set_count(n + p[P_KMINE])
+    glob.count += split
+    stats.reset(scene.count)
+    return DensifyEvent(step=step, eligible=p[P_ELIG], split=split, count_after=glob.count)
+
+
+def _split_guarded(scene, mask, guard, alpha, log_alpha, log_gamma, beta):
+    L = _lib.lib()
+    n = scene.count
+    ws = _lib.workspace(_lib.query_size(L.igs_las_workspace_bytes, n), scene.device, "las")
+    if hasattr(scene, "_rot"):
+        args = (scene._pos.data_ptr(), scene._ls.data_ptr(), scene._rot.data_ptr(),
+                scene._op.data_ptr(), scene._sh.data_ptr(), scene._sh.shape[1] * 3, 3)
+    else:
+        cols = scene._cols
+        args = (cols["positions"].data_ptr(), cols["log_scales"].data_ptr(),
+                cols["thetas"].data_ptr(), cols["opacity_logits"].data_ptr(),
+                cols["colors"].data_ptr(), 3, 2)
+    _lib.check(L.igs_las_split_guarded(*args, n, scene.reserved_rows, mask.data_ptr(), alpha,
+                                       log_alpha, log_gamma, beta, guard.data_ptr(),
+                                       ws.data_ptr(), ws.numel(), _lib.stream_handle()),
+               "densify_step_sharded")
 
 
 @dataclass
@@ -187,104 +382,90 @@ class ShardSplit:
         return sum(self.n_split)
 
 
-def _las_check_global(scene, summaries, caps, c):
-    """Host checks of las_split.py:146-155 over all ranks (every rank raises the same
-    error).  summaries: per rank (n_split, flags); caps: per rank (count, capacity)."""
-    for (ns, _), (cnt, cap) in zip(summaries, caps):
-        if cnt + ns > cap:
-            raise _las.BudgetError(f"splitting {ns} of {cnt} primitives exceeds shard capacity "
-                                   f"{cap}")
+def _las_check_global(summaries, count: int, capacity: int):
+    """The reference's checks (las_split.py:146-155) on the GLOBAL scene: one count and one
+    capacity (sums over the ranks), the domain flags of every rank's masked parents.
+    summaries: per rank (n_split, flags).  Every rank raises the same error."""
+    total = sum(ns for ns, _ in summaries)
+    if count + total > capacity:
+        raise _las.BudgetError(f"splitting {total} of {count} primitives exceeds capacity "
+                               f"{capacity}")
     flags = 0
     for ns, fl in summaries:
         if ns:
             flags |= fl
-    if flags & _lib.IGS_LAS_BAD_OPACITY:
+    if total and flags & _lib.IGS_LAS_BAD_OPACITY:
         raise ValueError("logit requires all values strictly inside (0, 1)")
-    if flags & _lib.IGS_LAS_BAD_QUAT:
+    if total and flags & _lib.IGS_LAS_BAD_QUAT:
         raise ValueError("zero or non-finite quaternion")
     return flags
 
 
-def las_split_sharded(scene: Scene3, mask, c: _las.SplitConstants = _las.SplitConstants(),
-                      comm: Comm | None = None, extra=None):
-    """Split this rank's masked parents of a contiguous shard in place (las_split.py:158-179
-    on the global cloud).  Returns a ShardSplit; ``extra`` (device int64 tensor) rides along
-    in the same all-gather (densify_step_sharded uses it for the eligible count)."""
+def las_split_sharded(scene, mask, c: _las.SplitConstants = _las.SplitConstants(),
+                      comm: Comm | None = None):
+    """Split this rank's masked parents in place (las_split.py:158-179 on the global cloud):
+    one all-gather of {n_split, flags, count, capacity}; children keep to their parents' rank
+    and get the global indices the reference gives them."""
     comm = comm or Comm()
+    glob = attach(scene, comm)
+    n = scene.count
     prep = _las.prepare(scene, mask, c)
-    cap = torch.tensor([scene.count, scene.capacity], dtype=torch.int64, device=scene.device)
-    parts = [prep.summary, cap] + ([extra] if extra is not None else [])
-    g = comm.all_gather(torch.cat(parts)).cpu().tolist()
+    caps_now = torch.tensor([scene.count, scene.capacity], dtype=torch.int64, device=scene.device)
+    g = comm.all_gather(torch.cat([prep.summary, caps_now])).cpu().tolist()
     summaries = [(int(r[0]), int(r[1])) for r in g]
     caps = [(int(r[2]), int(r[3])) for r in g]
-    flags = _las_check_global(scene, summaries, caps, c)
+    flags = _las_check_global(summaries, glob.count, glob.capacity)
     ns_local = summaries[comm.rank][0]
-    if ns_local:
-        # apply with this rank's own flags except the batch-global renormalisation bit
-        _las.check_and_apply(prep, ns_local, (flags & _lib.IGS_LAS_RENORM), c)
     n_split = [s[0] for s in summaries]
-    parents = [cp[0] for cp in caps]
-    offset = sum(parents) + sum(n_split[:comm.rank])
-    res = ShardSplit(n_split=n_split, parents=parents, flags=flags, offset=offset)
-    res.extra = [r[4:] for r in g]
-    return res
+    offset = glob.count + sum(n_split[:comm.rank])
+    if ns_local:
+        _reserve(scene, n + ns_local)           # the shard's share of the global headroom
+        scene._capacity = max(scene._capacity, n + ns_local)
+        _las.check_and_apply(prep, ns_local, flags & _lib.IGS_LAS_RENORM, c)
+        plan = torch.tensor([0, 0, STATUS_OK, 0, 0, offset, ns_local, 0] + [0] * 8,
+                            dtype=torch.int64, device=scene.device)
+        _lib.check(_lib.lib().igs_shard_child_index(scene._gidx.data_ptr(), n, plan.data_ptr(),
+                                                    _lib.stream_handle()), "las_split_sharded")
+    glob.count += sum(n_split)
+    return ShardSplit(n_split=n_split, parents=[cp[0] for cp in caps], flags=flags,
+                      offset=offset)
 
 
-def densify_step_sharded(scene: Scene3, stats: DensifyStats, cfg: DensifyConfig, step: int,
-                         comm: Comm | None = None, caps=None, select_ops=None):
-    """One densify event over a sharded cloud (densify_controller.py:125-147 on the global
-    scene).  Every rank returns the same DensifyEvent with global counts.  ``caps``: the
-    per-rank (count, capacity) list if the caller already has it (else one all-gather)."""
-    comm = comm or Comm()
-    if not is_densify_step(cfg, step):
-        raise ValueError(f"step {step} is not a densify step for this timetable")
-    if len(stats) != scene.count:
-        raise ValueError("stats length does not match scene count")
-    caps = caps or global_counts(scene, comm)
-    n_glob = sum(c for c, _ in caps)
-    headroom = sum(cap for _, cap in caps) - n_glob
-    take_cap = _take_cap(cfg, n_glob, headroom) if (headroom > 0 and n_glob > 0) else 0
-    ops = select_ops or CudaSelectShard(len(stats), stats._device)
-    mask, counts = select_shard_protocol(ops, stats, cfg, step, take_cap, comm)
-    if take_cap > 0:
-        res = las_split_sharded(scene, mask, cfg.split_constants, comm, extra=counts)
-        eligible = int(res.extra[0][0])
-        split = res.total
-    else:
-        g = counts.cpu().tolist()
-        eligible, split = int(g[0]), 0
-    stats.reset(scene.count)
-    count_after = n_glob + split
-    return DensifyEvent(step=step, eligible=eligible, split=split, count_after=count_after)
+_FIELDS = ("positions", "log_scales", "rotations", "opacity_logits", "sh")
 
 
-_FIELDS = (("_pos", 3), ("_ls", 3), ("_rot", 4), ("_op", 1))
-
-
-def gather_scene(scene: Scene3, parents_before: int, comm: Comm | None = None) -> dict:
-    """All-gather the shards into the reference's global layout on every rank: all ranks'
-    first ``parents_before`` rows (the parents, split in place), then all ranks' appended
-    children, in rank order.  Returns a dict of CUDA tensors (positions, log_scales,
-    rotations, opacity_logits, sh).  Rows are packed into one padded float32 block per
-    rank for a single all-gather."""
+def gather_scene(scene, parents_before: int | None = None, comm: Comm | None = None) -> dict:
+    """All-gather the shards into the reference's global layout on every rank: each row at
+    its global index.  Returns a dict of tensors (positions, log_scales, rotations,
+    opacity_logits, sh).  (``parents_before`` is accepted for compatibility; the global
+    indices carry the layout.)"""
     comm = comm or Comm()
     sh_f = scene._sh.shape[1] * 3
     width = 3 + 3 + 4 + 1 + sh_f
     n = scene.count
+    gidx = getattr(scene, "_gidx", None)
+    if gidx is None:  # a plain contiguous shard
+        sizes = comm.all_gather(torch.tensor([n], dtype=torch.int64, device=scene.device)).cpu()
+        lo = int(sizes[:comm.rank].sum())
+        gidx = torch.arange(lo, lo + n, dtype=torch.int64, device=scene.device)
     cols = [scene._pos[:n], scene._ls[:n], scene._rot[:n], scene._op[:n, None],
             scene._sh[:n].reshape(n, sh_f)]
-    meta = torch.tensor([n, parents_before], dtype=torch.int64, device=scene.device)
-    metas = comm.all_gather(meta).cpu().tolist()
-    rows = max(m[0] for m in metas)
-    block = torch.zeros((rows, width), dtype=torch.float32, device=scene.device)
-    block[:n] = torch.cat(cols, dim=1)
+    counts = comm.all_gather(torch.tensor([n], dtype=torch.int64, device=scene.device))
+    counts = counts.reshape(-1).cpu().tolist()
+    rows = max(counts)
+    block = torch.zeros((rows, width + 2), dtype=torch.float32, device=scene.device)
+    block[:n, :width] = torch.cat(cols, dim=1)
+    block[:n, width:] = gidx[:n].to(torch.int64).view(torch.int32).reshape(n, 2).view(
+        torch.float32)
     blocks = comm.all_gather(block)
-    parents = [blocks[r, :metas[r][1]] for r in range(comm.world)]
-    children = [blocks[r, metas[r][1]:metas[r][0]] for r in range(comm.world)]
-    full = torch.cat(parents + children)
+    total = sum(counts)
+    full = torch.empty((total, width), dtype=torch.float32, device=scene.device)
+    for r in range(comm.world):
+        b = blocks[r, :counts[r]]
+        idx = b[:, width:].contiguous().view(torch.int32).view(torch.int64).reshape(-1)
+        full[idx] = b[:, :width]
     out, o = {}, 0
-    for name, w in (("positions", 3), ("log_scales", 3), ("rotations", 4),
-                    ("opacity_logits", 1), ("sh", sh_f)):
+    for name, w in zip(_FIELDS, (3, 3, 4, 1, sh_f)):
         out[name] = full[:, o:o + w]
         o += w
     out["opacity_logits"] = out["opacity_logits"].reshape(-1)

@@ -1,16 +1,20 @@
-"""CPU test double of the per-rank sharded-select kernels (igs_select_shard_*), so the
-collective protocol in paper_2603_08661_b200.sharded can run under gloo on CPU.
-TEST INFRASTRUCTURE ONLY: the product path uses sharded.CudaSelectShard."""
+"""CPU test double of the per-rank sharded-step kernels (igs_shard_keys / _boundary /
+_finalize), so the collective protocol in paper_2603_08661_b200.sharded can run under gloo
+on CPU.  It restates the kernels' arithmetic in numpy (same digit, same records, same plan).
+TEST INFRASTRUCTURE ONLY: the product path uses sharded.CudaShardOps."""
 
 from __future__ import annotations
 
 import numpy as np
 import torch
 
+from paper_2603_08661_b200 import sharded as S
 from paper_2603_08661_b200.schedule import is_warmup_step
 
 NBINS = 1 << 16
 INELIGIBLE = np.uint64(0xFFFFFFFFFFFFFFFF)
+NAN_KEY = np.uint64(0xFFF8000000000000)
+T_LO, T_HI = 984064, 984064 + 65532
 
 
 def score_keys(score):
@@ -20,7 +24,17 @@ def score_keys(score):
     top = np.uint64(1) << np.uint64(63)
     u = np.where((b & top) != 0, ~b, b | top)
     k = ~u
-    return np.where(np.isnan(score), np.uint64(0xFFF8000000000000), k)
+    return np.where(np.isnan(score), NAN_KEY, k)
+
+
+def key_digit(k):
+    """select_shard.cu key_digit, vectorised."""
+    u = ~k
+    pos = (u >> np.uint64(63)) != 0
+    b = u & np.uint64(0x7FFFFFFFFFFFFFFF)
+    t = np.clip((b >> np.uint64(42)).astype(np.int64), T_LO, T_HI)
+    d = np.where(pos & (b != 0), 1 + (T_HI - t), 65534)
+    return np.where(k == NAN_KEY, 65535, d).astype(np.int64)
 
 
 class NumpyShardOps:
@@ -38,51 +52,60 @@ class NumpyShardOps:
             sc = g
         else:
             sc = e * g
-        k = score_keys(sc)
-        self.k = np.where(elig, k, INELIGIBLE)
+        self.k = np.where(elig, score_keys(sc), INELIGIBLE)
+        self.elig = elig
         hist = np.zeros(NBINS + 1, np.int64)
-        np.add.at(hist, (self.k[elig] >> np.uint64(48)).astype(np.int64), 1)
+        np.add.at(hist, key_digit(self.k[elig]), 1)
         hist[NBINS] = int(elig.sum())
         return torch.from_numpy(hist.astype(np.int32))
 
-    def resolve(self, hist, rnd, take_cap):
+    def boundary(self, hist, take_cap, gidx, scene, beta, cap):
         h = hist.cpu().numpy().astype(np.int64)
-        if rnd == 0:
-            ne = int(h[NBINS])
-            self.take = min(ne, take_cap)
-            self.counts = torch.tensor([ne, self.take], dtype=torch.int64)
-            self.prefix, self.pmask, self.rank = 0, 0, self.take - 1
-            self.status = 0 if self.take else 1
-        if self.status:
-            return self.counts
-        cum = np.cumsum(h[:NBINS])
-        d = int(np.searchsorted(cum, self.rank, side="right"))
-        self.rank -= int(cum[d - 1]) if d else 0
-        sh = 48 - 16 * rnd
-        self.prefix |= d << sh
-        self.pmask |= 0xFFFF << sh
-        if rnd == 3:
-            self.T = np.uint64(self.prefix)
-            self.need = self.rank + 1
-        return self.counts
+        ne = int(h[NBINS])
+        self.take = min(ne, int(take_cap))
+        self.n_elig = ne
+        self.B, self.need = NBINS, 0
+        if self.take:
+            cum = np.cumsum(h[:NBINS])
+            self.B = int(np.searchsorted(cum, self.take - 1, side="right"))
+            self.need = self.take - (int(cum[self.B - 1]) if self.B else 0)
+        rec = np.zeros(S.REC_HDR + 2 * cap, np.int64)
+        if self.take:
+            d = key_digit(self.k)
+            gi = gidx.cpu().numpy()
+            rec[0] = int((self.elig & (d < self.B)).sum())
+            sel = np.flatnonzero(self.elig & (d == self.B))
+            rec[1] = len(sel)
+            m = min(len(sel), cap)
+            rec[S.REC_HDR:S.REC_HDR + 2 * m:2] = self.k[sel[:m]].view(np.int64)
+            rec[S.REC_HDR + 1:S.REC_HDR + 2 * m:2] = gi[sel[:m]]
+        return torch.from_numpy(rec)
 
-    def digit_hist(self, rnd):
-        hist = np.zeros(NBINS + 1, np.int64)
-        if not self.status:
-            sel = (self.k != INELIGIBLE) & ((self.k & np.uint64(self.pmask)) == np.uint64(self.prefix))
-            d = ((self.k[sel] >> np.uint64(48 - 16 * rnd)) & np.uint64(0xFFFF)).astype(np.int64)
-            np.add.at(hist, d, 1)
-        return torch.from_numpy(hist.astype(np.int32))
-
-    def ties(self):
-        c = 0 if self.status else int((self.k == self.T).sum())
-        return torch.tensor([c], dtype=torch.int64)
-
-    def finalize(self, all_ties, rank):
-        if self.status:
-            return torch.zeros(self.n, dtype=torch.bool)
-        before = int(all_ties.reshape(-1)[:rank].sum())
-        tie = self.k == self.T
-        tie_rank = before + np.cumsum(tie) - tie
-        m = (self.k < self.T) | (tie & (tie_rank < self.need))
-        return torch.from_numpy(m)
+    def finalize(self, records, rank, cap, n_global, gidx):
+        recs = records.cpu().numpy().reshape(records.shape[0], -1)
+        plan = np.zeros(S.PLAN_WORDS, np.int64)
+        plan[S.P_TAKE], plan[S.P_ELIG] = self.take, self.n_elig
+        plan[S.P_MAXB] = int(recs[:, 1].max())
+        mask = np.zeros(self.n, bool)
+        if not self.take:
+            plan[S.P_STATUS] = S.STATUS_NOTHING
+        elif (recs[:, 1] > cap).any():
+            plan[S.P_STATUS] = S.STATUS_OVERFLOW
+        else:
+            keys, gix, owner = [], [], []
+            for r, rec in enumerate(recs):
+                m = int(rec[1])
+                keys.append(rec[S.REC_HDR:S.REC_HDR + 2 * m:2].view(np.uint64))
+                gix.append(rec[S.REC_HDR + 1:S.REC_HDR + 2 * m:2] & ((1 << 56) - 1))
+                owner.append(np.full(m, r))
+            keys, gix, owner = map(np.concatenate, (keys, gix, owner))
+            order = np.lexsort((gix, keys))[:self.need]
+            T, G = keys[order[-1]], gix[order[-1]]
+            k_r = recs[:, 0] + np.bincount(owner[order], minlength=len(recs))
+            plan[S.P_NSPLIT] = plan[S.P_KMINE] = k_r[rank]
+            plan[S.P_CHILD] = n_global + int(k_r[:rank].sum())
+            d = key_digit(self.k)
+            gi = gidx.cpu().numpy()
+            mask = self.elig & ((d < self.B) | ((d == self.B) & (
+                (self.k < T) | ((self.k == T) & (gi <= G)))))
+        return torch.from_numpy(mask.astype(np.uint8)), torch.from_numpy(plan)

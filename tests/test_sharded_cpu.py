@@ -1,7 +1,8 @@
 """Multi-rank protocol of the sharded densification path on CPU: world_size 2 (and 3) over
 gloo, the per-rank kernels replaced by a numpy test double (tests/shard_double.py).
-Checks that the collective schedule of sharded.select_shard_protocol reproduces the
-single-process oracle selection bit-for-bit, and the host-side global checks / gather."""
+Checks that the two-round collective schedule of sharded.select_candidates_sharded (including
+the boundary-bucket overflow re-run) reproduces the single-process oracle selection
+bit-for-bit, the global budget checks and the gather by global index."""
 
 import os
 import socket
@@ -45,8 +46,7 @@ def _worker(rank, world, port, cases, q):
 
 
 def _one(rank, world, case, sharded, DensifyStats, DensifyConfig, NumpyShardOps):
-    from paper_2603_08661_b200.densify_controller import _take_cap
-    grad, edge, step, policy, cap, headroom = case
+    grad, edge, step, policy, cap, headroom, rcap = case
     n = len(grad)
     lo, hi = sharded.shard_range(n, rank, world)
     st = DensifyStats(hi - lo, device="cpu")
@@ -55,13 +55,13 @@ def _one(rank, world, case, sharded, DensifyStats, DensifyConfig, NumpyShardOps)
     st.edge_score.copy_(torch.from_numpy(edge[lo:hi]))
     cfg = DensifyConfig(budget=10 * n, growth_cap=cap, policy=policy)
     comm = sharded.Comm()
-    take_cap = _take_cap(cfg, n, headroom) if headroom > 0 else 0
-    mask, counts = sharded.select_shard_protocol(NumpyShardOps(hi - lo), st, cfg, step,
-                                                 take_cap, comm)
+    mask, plan = sharded.select_candidates_sharded(st, cfg, step, headroom, n, comm,
+                                                   ops=NumpyShardOps(hi - lo), record_cap=rcap,
+                                                   return_plan=True)
     m = torch.zeros(n, dtype=torch.uint8)
     m[lo:hi] = mask.to(torch.uint8)
     dist.all_reduce(m)
-    return (rank, m.numpy().astype(bool), counts.tolist())
+    return (rank, m.numpy().astype(bool), [plan[sharded.P_ELIG], plan[sharded.P_TAKE]])
 
 
 _RESULTS = {}
@@ -91,18 +91,25 @@ for _n, _tied in ((1001, False), (4000, True), (17, True)):
     e = _rng.random(_n)
     if _tied:
         g, e = np.round(g, 4), np.round(e, 1)
-    CASES.append((g, e, 2000, "product", 0.05, _n))
-    CASES.append((g, e, 500, "product", 0.3, _n // 3))
-    CASES.append((g, e, 2000, "grad", 1.0, _n))
-# all ties and no eligible
-CASES.append((np.full(999, 3e-4), np.full(999, 0.5), 2000, "product", 0.5, 999))
-CASES.append((np.full(50, 1e-6), np.full(50, 0.5), 2000, "product", 0.5, 50))
+    CASES.append((g, e, 2000, "product", 0.05, _n, None))
+    CASES.append((g, e, 500, "product", 0.3, _n // 3, None))
+    CASES.append((g, e, 2000, "grad", 1.0, _n, None))
+    CASES.append((g, e, 2000, "product", 0.3, _n, 2))  # boundary bucket overflows the records
+# all ties (the boundary bucket is every eligible score), with and without the overflow
+# re-run, and no eligible
+CASES.append((np.full(999, 3e-4), np.full(999, 0.5), 2000, "product", 0.5, 999, None))
+CASES.append((np.full(999, 3e-4), np.full(999, 0.5), 2000, "product", 0.5, 999, 16))
+CASES.append((np.full(50, 1e-6), np.full(50, 0.5), 2000, "product", 0.5, 50, None))
+# scores outside the digit's fine range, negatives, zeros
+_g = _rng.exponential(2e-4, 600)
+_e = np.concatenate([np.full(100, 1e30), np.full(100, -2.0), np.zeros(100), _rng.random(300)])
+CASES.append((_g, _e, 2000, "edge", 0.5, 600, None))
 
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("ci", range(len(CASES)))
 def test_sharded_select_protocol_matches_single_process(world, ci):
-    grad, edge, step, policy, cap, headroom = CASES[ci]
+    grad, edge, step, policy, cap, headroom, _ = CASES[ci]
     res = [r[1:] for r in _run(world, CASES) if r[0] == ci]
     assert len(res) == world
     warm = OS.is_warmup_step(500, 15000, 500, 3, step)
@@ -128,20 +135,23 @@ def test_shard_range_covers_contiguously():
 
 
 def test_global_las_checks():
+    """One global capacity, as the reference's las_split_batch (las_split.py:146-155): a
+    selection that piles onto one shard past its local share still fits the global budget."""
     from paper_2603_08661_b200 import _lib, sharded
-    from paper_2603_08661_b200.las_split import BudgetError, SplitConstants
-    c = SplitConstants()
-    caps = [(10, 20), (10, 12)]
-    assert sharded._las_check_global(None, [(5, 0), (2, 0)], caps, c) == 0
+    from paper_2603_08661_b200.las_split import BudgetError
+    # two shards of 10 rows, global capacity 32: 5 + 3 splits fit, although shard 1 alone
+    # reserved only 12 rows
+    assert sharded._las_check_global([(5, 0), (3, 0)], 20, 32) == 0
+    assert sharded._las_check_global([(8, 0), (4, 0)], 20, 32) == 0
     with pytest.raises(BudgetError):
-        sharded._las_check_global(None, [(5, 0), (3, 0)], caps, c)
+        sharded._las_check_global([(8, 0), (5, 0)], 20, 32)
     # renormalisation is batch-global: one rank's flag applies to every rank
-    assert sharded._las_check_global(None, [(1, _lib.IGS_LAS_RENORM), (1, 0)], caps, c) == \
+    assert sharded._las_check_global([(1, _lib.IGS_LAS_RENORM), (1, 0)], 20, 32) == \
         _lib.IGS_LAS_RENORM
     # flags of a rank that splits nothing do not count (its masked batch is empty)
-    assert sharded._las_check_global(None, [(0, _lib.IGS_LAS_BAD_QUAT), (1, 0)], caps, c) == 0
+    assert sharded._las_check_global([(0, _lib.IGS_LAS_BAD_QUAT), (1, 0)], 20, 32) == 0
     with pytest.raises(ValueError):
-        sharded._las_check_global(None, [(1, _lib.IGS_LAS_BAD_QUAT), (1, 0)], caps, c)
+        sharded._las_check_global([(1, _lib.IGS_LAS_BAD_QUAT), (1, 0)], 20, 32)
 
 
 def _gather_worker(rank, world, port, q):
@@ -151,14 +161,19 @@ def _gather_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2603_08661_b200 import sharded
-        # rank r holds parents [r*10, r*10 + 3 + r) then 2 appended children
+        # rank r holds its parents (3 + r rows) then 2 appended children; global indices as
+        # the reference lays them out: parents of rank 0, of rank 1, then children in order
         parents = 3 + rank
         n = parents + 2
         rows = torch.arange(n, dtype=torch.float32) + 100 * rank
+        plo = 0 if rank == 0 else 3
+        clo = 7 + 2 * rank
+        gidx = torch.tensor(list(range(plo, plo + parents)) + [clo, clo + 1])
         sc = types.SimpleNamespace(
             _pos=rows[:, None].repeat(1, 3), _ls=rows[:, None].repeat(1, 3),
             _rot=rows[:, None].repeat(1, 4), _op=rows.clone(),
-            _sh=rows[:, None, None].repeat(1, 2, 3), count=n, device=torch.device("cpu"))
+            _sh=rows[:, None, None].repeat(1, 2, 3), count=n, device=torch.device("cpu"),
+            _gidx=gidx)
         out = sharded.gather_scene(sc, parents, sharded.Comm())
         q.put((rank, out["opacity_logits"].numpy().tolist(), tuple(out["sh"].shape)))
     finally:

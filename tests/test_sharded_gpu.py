@@ -1,4 +1,4 @@
-"""GPU parity of the sharded densification path (igs_select_shard_* + las on shards).
+"""GPU parity of the sharded densification path (igs_shard_* + the guarded split on shards).
 
 * world 1 (no process group): the sharded radix select through the real CUDA kernels equals
   the single-launch select and the oracle, bit for bit;
@@ -98,6 +98,96 @@ def _worker(rank, world, port, n, q, backend="gloo"):
                {kk: v.cpu().numpy() for kk, v in full.items()}))
     finally:
         dist.destroy_process_group()
+
+
+def _worker_events(rank, world, port, n, q, skew):
+    """Two consecutive densify events on the shards (the second one's ties break by the
+    global indices the first one gave the children); `skew`: every high score on rank 0,
+    whose own rows are too few to hold its children -- the global capacity still does."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2603_08661_b200 as b
+        from paper_2603_08661_b200 import sharded
+        pos, ls, qq, o, sh, grads, edges = _event_inputs(n, skew)
+        lo, hi = sharded.shard_range(n, rank, world)
+        k = hi - lo
+        cap = k + (n // 8 if skew else k)   # the shards' reservations differ from the global one
+        scene = b.Scene3(pos[lo:hi], ls[lo:hi], qq[lo:hi], o[lo:hi], sh[lo:hi], capacity=cap)
+        caps = sharded.global_counts(scene, sharded.Comm())
+        glob_cap = 3 * n
+        caps = [(c, glob_cap // world + (glob_cap % world if r == 0 else 0))
+                for r, (c, _) in enumerate(caps)]
+        cfg = b.DensifyConfig(budget=glob_cap, growth_cap=0.3)
+        evs = []
+        for step, (grad, edge) in zip((2000, 2500), zip(grads, edges)):
+            gi = scene._gidx[:scene.count].cpu().numpy() if hasattr(scene, "_gidx") else \
+                np.arange(lo, hi)
+            st = _stats(b, grad[gi], 1, edge[gi])
+            ev = sharded.densify_step_sharded(scene, st, cfg, step, caps=caps)
+            evs.append((ev.step, ev.eligible, ev.split, ev.count_after))
+            if step == 2000:   # the children follow the reference's numbering after event 1
+                full1 = sharded.gather_scene(scene)
+                q.put(("event1", rank, {kk: v.cpu().numpy() for kk, v in full1.items()}))
+                sharded.reshard(scene)
+        full = sharded.gather_scene(scene)
+        q.put((rank, evs, {kk: v.cpu().numpy() for kk, v in full.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def _event_inputs(n, skew):
+    pos, ls, qq, o, sh = _cloud(n, 21)
+    rng = np.random.default_rng(22)
+    total = n + int(np.ceil(0.3 * n)) + 10
+    grads = [rng.exponential(3e-4, total), rng.exponential(3e-4, total)]
+    edges = [np.round(rng.random(total), 1), np.round(rng.random(total), 1)]  # many ties
+    if skew:
+        for e in edges:
+            e[: n // 2] += 2.0     # the first half of the global array (rank 0) wins
+    return pos, ls, qq, o, sh, grads, edges
+
+
+@pytest.mark.parametrize("skew", [False, True])
+def test_sharded_two_events_match_single_device(skew):
+    import paper_2603_08661_b200 as b
+    n, world = 9_001, 2
+    pos, ls, qq, o, sh, grads, edges = _event_inputs(n, skew)
+    scene = b.Scene3(pos, ls, qq, o, sh, capacity=3 * n)
+    cfg = b.DensifyConfig(budget=3 * n, growth_cap=0.3)
+    want_ev, want1 = [], None
+    for step, (grad, edge) in zip((2000, 2500), zip(grads, edges)):
+        st = _stats(b, grad[:scene.count], 1, edge[:scene.count])
+        ev = b.densify_step(scene, st, cfg, step)
+        want_ev.append((ev.step, ev.eligible, ev.split, ev.count_after))
+        if want1 is None:
+            want1 = scene.to_numpy()
+    want = scene.to_numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_events, args=(r, world, port, n, q, skew))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2 * world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for item in res:
+        if item[0] == "event1":
+            _, rank, full = item
+            ref = want1
+        else:
+            rank, evs, full = item
+            assert evs == want_ev, rank
+            ref = want
+        for col in ("positions", "log_scales", "rotations", "opacity_logits", "sh"):
+            np.testing.assert_array_equal(full[col], ref[col], err_msg=f"{col} rank {rank}")
 
 
 @pytest.mark.parametrize("world,backend", [(2, "gloo"), (1, "nccl")])
