@@ -825,6 +825,7 @@ def bench_densify_sharded(args, world, rank, dev):
             getattr(scene, name)[:k].copy_(v)
         scene._set_count(k)
         sharded.detach(scene)   # the restored cloud is again a contiguous shard
+        sharded.attach(scene, comm, caps)
         stats = igs.DensifyStats(k, device=dev)
         stats._grad_sum.copy_(grad_t)
         stats._accum_count = 1

@@ -152,7 +152,10 @@ int igs_accumulate_grad_norms(double* grad_sum, const void* grads, int dtype, in
  * flags, [2] status (0 ok, 1 nothing selected, 2 boundary bucket larger than record_cap:
  * nothing split, re-run boundary/gather/finalize with record_cap >= plan[7]), [3] global
  * split count, [4] global eligible count, [5] global index of this rank's first child,
- * [6] this rank's split count, [7] largest boundary-bucket count over the ranks. */
+ * [6] this rank's split count, [7] largest boundary-bucket count over the ranks, [8] threshold
+ * key, [9] threshold global index, [10] boundary digit, [11] boundary entries to take.  With
+ * more than 32768 boundary entries over all ranks igs_shard_finalize sets status 2 as well
+ * and the caller selects from the gathered records itself, then calls igs_shard_mask. */
 #define IGS_SHARD_HIST_LEN 65537
 int igs_shard_workspace_bytes(int64_t n, size_t* bytes);
 int igs_shard_keys(const double* grad_sum, int64_t accum_count, const double* edge_score,
@@ -166,6 +169,10 @@ int igs_shard_finalize(const int64_t* records, int world, int rank, int64_t reco
                        int64_t n_global, const int64_t* gidx, int64_t n, uint8_t* mask,
                        int64_t* plan, void* workspace, size_t workspace_bytes, void* stream);
 int igs_shard_child_index(int64_t* gidx, int64_t count, const int64_t* plan, void* stream);
+/* This rank's mask for a plan computed outside igs_shard_finalize (the path for boundary
+ * buckets of more than 32768 entries over all ranks, e.g. every score equal). */
+int igs_shard_mask(const int64_t* gidx, int64_t n, const int64_t* plan, uint8_t* mask,
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- Long-Axis-Split (las_split.py:146-179) ----------------------------- */
 

@@ -55,6 +55,7 @@ SIGNATURES = {
     "igs_shard_finalize": (_int, [_vp, _int, _int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _sz,
                                   _vp]),
     "igs_shard_child_index": (_int, [_vp, _i64, _vp, _vp]),
+    "igs_shard_mask": (_int, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "igs_las_workspace_bytes": (_int, [_i64, _szp]),
     "igs_las_prepare": (_int, [_vp, _vp, _vp, _i64, _flt, _vp, _sz, _vp, _vp]),
     "igs_las_apply": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt, _flt,

@@ -180,28 +180,32 @@ __global__ void __launch_bounds__(NT) resolve_kernel(const int* __restrict__ his
     s_need = 0;
   }
   const int4* h4 = reinterpret_cast<const int4*>(hist) + threadIdx.x * 16;
+  int4 hv[16];
   unsigned sum = 0;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int4 v = __ldcg(h4 + k);
-    sum += (unsigned)v.x + (unsigned)v.y + (unsigned)v.z + (unsigned)v.w;
-  }
+  for (int k = 0; k < 16; ++k) hv[k] = __ldcg(h4 + k);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) sum += (unsigned)hv[k].x + (unsigned)hv[k].y + (unsigned)hv[k].z + (unsigned)hv[k].w;
   unsigned total;
   const unsigned before = block_exclusive_scan(sum, warp_sums, &total);
   if (take > 0) {
     const unsigned long long r = take - 1;
     if (r >= before && r < (unsigned long long)before + sum) {
       unsigned long long cum = before;
-      const int* hb = hist + threadIdx.x * 64;
-      for (int k = 0; k < 64; ++k) {
-        const unsigned c = (unsigned)__ldcg(hb + k);
-        if (r < cum + c) {
-          s_B = threadIdx.x * 64 + k;
-          s_need = take - cum;
-          break;
+      int found = -1;
+      unsigned long long at = 0;
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {  // the owner's bins are in its registers
+        const int4 v = hv[k >> 2];
+        const unsigned c = (unsigned)((k & 3) == 0 ? v.x : (k & 3) == 1 ? v.y : (k & 3) == 2 ? v.z : v.w);
+        if (found < 0 && r < cum + c) {
+          found = k;
+          at = cum;
         }
         cum += c;
       }
+      s_B = threadIdx.x * 64 + found;
+      s_need = take - at;
     }
   }
   __syncthreads();
@@ -301,29 +305,41 @@ enum Plan {
   P_T = 8,        // threshold key
   P_G = 9,        // threshold global index (key == T and gidx <= G is in)
   P_B = 10,       // boundary digit
+  P_NEED = 11,    // boundary entries to take
   P_WORDS = 16
 };
 constexpr int MAX_WORLD = 64;
+constexpr int EMAX = 8;             // boundary entries per thread in final_kernel
+constexpr long long MAX_ENTRIES = (long long)EMAX * NT;  // world * record_cap
 
-// Radix select (RBITS-bit digits, block-wide) of the rank-`rank` smallest value of f(e)
-// over entries e whose value matches `prefix` on `pmask`; returns the full value.
-template <typename F>
-__device__ unsigned long long block_select64(F f, long long m, unsigned long long rank,
-                                            unsigned* h, unsigned* warp_sums,
-                                            unsigned long long* s_val, int* s_bin,
-                                            unsigned long long prefix = 0,
-                                            unsigned long long pmask = 0) {
-  for (int top = 63; top >= 0; top -= RBITS) {
+// Radix select (RBITS-bit digits, block-wide) of the rank-`rank` smallest of the values v[k]
+// (ok[k]) each thread holds (E per thread); bits above `top` are equal in every value.
+template <int E>
+__device__ unsigned long long block_select64(const unsigned long long (&v)[E], const bool (&ok)[E],
+                                            unsigned long long rank, int top, unsigned* h,
+                                            unsigned* warp_sums, unsigned long long* s_val,
+                                            int* s_bin) {
+  unsigned long long prefix = 0, pmask = top >= 63 ? 0ull : (~0ull << (top + 1));
+  {  // the common high bits: any valid value
+    __shared__ unsigned long long s_any;
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (ok[k]) s_any = v[k];  // benign race: every writer stores a valid value
+    __syncthreads();
+    prefix = s_any & pmask;
+    __syncthreads();
+  }
+  for (; top >= 0; top -= RBITS) {
     const int width = top + 1 < RBITS ? top + 1 : RBITS;
     const int shift = top + 1 - width;
     const unsigned dmask = (1u << width) - 1;
     for (int i = threadIdx.x; i < RBINS; i += NT) h[i] = 0;
     __syncthreads();
-    for (long long e = threadIdx.x; e < m; e += NT) {
-      bool ok;
-      const unsigned long long v = f(e, ok);
-      if (ok && (v & pmask) == prefix) atomicAdd(&h[(v >> shift) & dmask], 1u);
-    }
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (ok[k] && (v[k] & pmask) == prefix) atomicAdd(&h[(v[k] >> shift) & dmask], 1u);
     __syncthreads();
     // RBINS / NT bins per thread, block scan, the owner of `rank` publishes the digit
     constexpr int PER = RBINS / NT;
@@ -377,31 +393,51 @@ __global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__
     plan[P_ELIG] = (long long)st->n_elig;
     plan[P_MAXB] = maxb;
     plan[P_B] = (long long)st->B;
+    plan[P_NEED] = (long long)need;
   }
-  if (st->status || overflow) {
+  if (st->status || overflow || world * cap > MAX_ENTRIES) {
     if (threadIdx.x == 0) plan[P_STATUS] = st->status ? 1 : 2;
     return;
   }
   const long long m = world * cap;  // entry e: rank e / cap, slot e % cap
-  auto key_of = [&](long long e, bool& ok) -> unsigned long long {
+  // every entry in registers: thread t holds entries t + NT k
+  unsigned long long kv[EMAX], gv[EMAX];
+  bool ok[EMAX];
+  unsigned long long kmin = ~0ull, kmax = 0;
+#pragma unroll
+  for (int k = 0; k < EMAX; ++k) {
+    const long long e = threadIdx.x + (long long)NT * k;
     const long long r = e / cap, s = e - r * cap;
-    ok = s < records[r * stride + R_BCNT];
-    return ok ? (unsigned long long)records[r * stride + R_HDR + 2 * s] : 0ull;
-  };
-  // threshold key T: the need-th smallest boundary key (rank need - 1)
-  const unsigned long long T = block_select64(key_of, m, need - 1, h, warp_sums, &s_val,
-                                              &s_bin);
-  // ties on T: how many of them are in, and the gidx cutoff when not all are
-  __syncthreads();
-  unsigned long long below = 0, ties = 0;
-  for (long long e = threadIdx.x; e < m; e += NT) {
-    bool ok;
-    const unsigned long long k = key_of(e, ok);
-    if (ok) {
-      below += k < T;
-      ties += k == T;
+    ok[k] = e < m && s < records[r * stride + R_BCNT];
+    kv[k] = ok[k] ? (unsigned long long)records[r * stride + R_HDR + 2 * s] : 0ull;
+    gv[k] = ok[k] ? (unsigned long long)records[r * stride + R_HDR + 2 * s + 1] : 0ull;
+    if (ok[k]) {
+      kmin = kv[k] < kmin ? kv[k] : kmin;
+      kmax = kv[k] > kmax ? kv[k] : kmax;
     }
   }
+  // the boundary keys share their high bits (one digit bucket): start below them
+  __shared__ unsigned long long s_min, s_max;
+  if (threadIdx.x == 0) {
+    s_min = ~0ull;
+    s_max = 0;
+  }
+  __syncthreads();
+  atomicMin(&s_min, kmin);
+  atomicMax(&s_max, kmax);
+  __syncthreads();
+  const unsigned long long diff = s_min ^ s_max;
+  const int top = diff ? 63 - __clzll(diff) : 0;
+  // threshold key T: the need-th smallest boundary key (rank need - 1)
+  const unsigned long long T = block_select64<EMAX>(kv, ok, need - 1, top, h, warp_sums, &s_val,
+                                                    &s_bin);
+  unsigned long long below = 0, ties = 0;
+#pragma unroll
+  for (int k = 0; k < EMAX; ++k)
+    if (ok[k]) {
+      below += kv[k] < T;
+      ties += kv[k] == T;
+    }
   for (int o = 16; o; o >>= 1) {
     below += __shfl_down_sync(0xffffffffu, below, o);
     ties += __shfl_down_sync(0xffffffffu, ties, o);
@@ -420,15 +456,14 @@ __global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__
   const unsigned long long need_ties = need - s_below;
   unsigned long long G = 0x00FFFFFFFFFFFFFFull;  // every tie in
   if (need_ties < s_ties) {
-    auto gidx_of = [&](long long e, bool& ok) -> unsigned long long {
-      const long long r = e / cap, s = e - r * cap;
-      ok = s < records[r * stride + R_BCNT] &&
-           (unsigned long long)records[r * stride + R_HDR + 2 * s] == T;
-      return ok ? ((unsigned long long)records[r * stride + R_HDR + 2 * s + 1] &
-                   0x00FFFFFFFFFFFFFFull)
-                : 0ull;
-    };
-    G = block_select64(gidx_of, m, need_ties - 1, h, warp_sums, &s_val, &s_bin);
+    unsigned long long gi[EMAX];
+    bool tie[EMAX];
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+      tie[k] = ok[k] && kv[k] == T;
+      gi[k] = gv[k] & 0x00FFFFFFFFFFFFFFull;
+    }
+    G = block_select64<EMAX>(gi, tie, need_ties - 1, 55, h, warp_sums, &s_val, &s_bin);
   }
   // every rank's split count and the batch flags
   for (int r = threadIdx.x; r < world; r += NT)
@@ -438,16 +473,14 @@ __global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__
     for (int r = 0; r < world; ++r) s_flags |= (unsigned)records[r * stride + R_LTFLAGS];
   }
   __syncthreads();
-  for (long long e = threadIdx.x; e < m; e += NT) {
-    bool ok;
-    const unsigned long long k = key_of(e, ok);
-    if (!ok) continue;
-    const long long r = e / cap, s = e - r * cap;
-    const unsigned long long w = (unsigned long long)records[r * stride + R_HDR + 2 * s + 1];
-    const unsigned long long g = w & 0x00FFFFFFFFFFFFFFull;
-    if (k < T || (k == T && g <= G)) {
-      atomicAdd(&s_k[r], 1ull);
-      atomicOr(&s_flags, (unsigned)(w >> 56));
+#pragma unroll
+  for (int k = 0; k < EMAX; ++k) {
+    if (!ok[k]) continue;
+    const unsigned long long g = gv[k] & 0x00FFFFFFFFFFFFFFull;
+    if (kv[k] < T || (kv[k] == T && g <= G)) {
+      const long long e = threadIdx.x + (long long)NT * k;
+      atomicAdd(&s_k[e / cap], 1ull);
+      atomicOr(&s_flags, (unsigned)(gv[k] >> 56));
     }
   }
   __syncthreads();
@@ -551,7 +584,11 @@ int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64
   shard::resolve_kernel<<<1, shard::NT, 0, st>>>(global_hist, take_cap, S, (long long*)record);
   IGS_LAUNCH_CHECK();
   if (n == 0) return IGS_OK;
-  shard::compact_kernel<<<shard::grid_for(n), shard::NT, 0, st>>>(
+  long long cgrid = (n + shard::NT * shard::U - 1) / (shard::NT * shard::U);
+  const long long cmax = 2LL * (sm_count() > 0 ? sm_count() : 148);
+  if (cgrid > cmax) cgrid = cmax;
+  if (cgrid < 1) cgrid = 1;
+  shard::compact_kernel<<<(unsigned)cgrid, shard::NT, 0, st>>>(
       (const unsigned long long*)(w + L.keys), (const long long*)gidx, rotations, opacity_logits,
       beta, n, S, record_cap, (long long*)record);
   IGS_LAUNCH_CHECK();
@@ -580,6 +617,23 @@ int igs_shard_finalize(const int64_t* records, int world, int rank, int64_t reco
   if (grid > cap) grid = cap;
   shard::mask_kernel<<<(unsigned)grid, shard::NT, 0, st>>>(
       (const unsigned long long*)(w + L.keys), (const long long*)gidx, n,
+      (const long long*)plan, mask);
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
+// The mask of a plan computed elsewhere (the large-boundary-bucket path).
+int igs_shard_mask(const int64_t* gidx, int64_t n, const int64_t* plan, uint8_t* mask,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+  if (!plan || n < 0 || (n > 0 && (!gidx || !mask))) return IGS_ERR_ARGUMENT;
+  if (n == 0) return IGS_OK;
+  shard::Layout L = shard::layout(n);
+  if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
+  long long grid = (n + shard::NT - 1) / shard::NT;
+  const long long cap = 8LL * (sm_count() > 0 ? sm_count() : 148);
+  if (grid > cap) grid = cap;
+  shard::mask_kernel<<<(unsigned)grid, shard::NT, 0, (cudaStream_t)stream>>>(
+      (const unsigned long long*)((char*)workspace + L.keys), (const long long*)gidx, n,
       (const long long*)plan, mask);
   IGS_LAUNCH_CHECK();
   return IGS_OK;

@@ -60,9 +60,10 @@ from .densify_controller import DensifyEvent, DensifyStats, _take_cap
 from .schedule import DensifyConfig, is_densify_step, is_warmup_step
 
 REC_HDR = 4                  # record header words: #(digit < B), boundary count, their flags, 0
-DEFAULT_RECORD_CAP = 4096    # boundary entries per rank per record (two int64 words each)
+MAX_ENTRIES = 8192           # boundary entries over all ranks that igs_shard_finalize selects
 PLAN_WORDS = 16
 P_NSPLIT, P_FLAGS, P_STATUS, P_TAKE, P_ELIG, P_CHILD, P_KMINE, P_MAXB = range(8)
+P_T, P_G, P_B, P_NEED = 8, 9, 10, 11
 STATUS_OK, STATUS_NOTHING, STATUS_OVERFLOW = 0, 1, 2
 
 
@@ -121,6 +122,17 @@ class CudaShardOps:
         self.hist = torch.empty(_lib.IGS_SHARD_HIST_LEN + 3, dtype=torch.int32,
                                 device=self.device)[:_lib.IGS_SHARD_HIST_LEN]
         self.plan = torch.zeros(PLAN_WORDS, dtype=torch.int64, device=self.device)
+        self.mask = torch.empty(self.n, dtype=torch.uint8, device=self.device)
+        self.records = {}
+
+    @classmethod
+    def cached(cls, owner, n: int, device):
+        """One instance per (owner object, n): the buffers are reused event after event."""
+        ops = getattr(owner, "_shard_ops", None)
+        if ops is None or ops.n != n or ops.device != torch.device(device):
+            ops = cls(n, device)
+            owner._shard_ops = ops
+        return ops
 
     def keys(self, stats: DensifyStats, cfg: DensifyConfig, step: int) -> torch.Tensor:
         _lib.check(self.L.igs_shard_keys(
@@ -131,7 +143,10 @@ class CudaShardOps:
         return self.hist
 
     def boundary(self, hist, take_cap: int, gidx, scene, beta: float, cap: int):
-        rec = torch.empty(REC_HDR + 2 * cap, dtype=torch.int64, device=self.device)
+        rec = self.records.get(cap)
+        if rec is None:
+            rec = self.records[cap] = torch.empty(REC_HDR + 2 * cap, dtype=torch.int64,
+                                                  device=self.device)
         rot, op = _flag_columns(scene)
         _lib.check(self.L.igs_shard_boundary(
             hist.data_ptr(), int(take_cap), gidx.data_ptr(), rot, op, float(beta), self.n,
@@ -140,7 +155,7 @@ class CudaShardOps:
         return rec
 
     def finalize(self, records, rank: int, cap: int, n_global: int, gidx):
-        mask = torch.empty(self.n, dtype=torch.uint8, device=self.device)
+        mask = self.mask
         records = records.contiguous()
         _lib.check(self.L.igs_shard_finalize(
             records.data_ptr(), records.shape[0], rank, int(cap), int(n_global),
@@ -179,8 +194,64 @@ def _read(plan, pinned):
     return [int(v) for v in view]
 
 
-def _overflow_cap(maxb: int) -> int:
-    return max(DEFAULT_RECORD_CAP, 1 << math.ceil(math.log2(max(maxb, 1))))
+def default_record_cap(world: int) -> int:
+    """Boundary entries per rank per record: the kernel's selection capacity split over the
+    ranks (a 65536-bin digit leaves ~10^3 scores in the boundary bucket of a 6M cloud)."""
+    return max(64, MAX_ENTRIES // max(world, 1))
+
+
+def _final_large(ops, records, comm, cap, n_global, gidx):
+    """The selection for boundary buckets of more than MAX_ENTRIES entries over all ranks (a
+    degenerate score distribution, e.g. every warm-up edge score 0): every record holds the
+    whole bucket; a stable device sort by (key, gidx) replaces final_kernel's radix select,
+    then igs_shard_mask.  Same plan, same result; costs host reads."""
+    recs = records.reshape(comm.world, -1)
+    plan = ops.plan
+    hdr = recs[:, :REC_HDR].cpu().tolist()
+    need = int(plan[P_NEED])
+    keys, gix, owner = [], [], []
+    for r, h in enumerate(hdr):
+        m = int(h[1])
+        e = recs[r, REC_HDR:REC_HDR + 2 * m].reshape(m, 2)
+        keys.append(e[:, 0])
+        gix.append(e[:, 1])
+        owner.append(torch.full((m,), r, dtype=torch.int64, device=recs.device))
+    keys, gix, owner = torch.cat(keys), torch.cat(gix), torch.cat(owner)
+    flags_e = gix >> 56
+    g = gix & ((1 << 56) - 1)
+    signed = keys ^ (-(2 ** 63))             # unsigned order as signed int64
+    o = torch.sort(g, stable=True).indices
+    o = o[torch.sort(signed[o], stable=True).indices][:need]
+    lt = torch.tensor([h[0] for h in hdr], dtype=torch.int64, device=recs.device)
+    k_r = lt + torch.bincount(owner[o], minlength=comm.world)
+    fl = 0
+    for h in hdr:
+        fl |= int(h[2])
+    for v in flags_e[o].unique().tolist():
+        fl |= int(v)
+    kr = k_r.cpu().tolist()
+    last = o[-1]
+    vals = {P_NSPLIT: kr[comm.rank], P_FLAGS: fl, P_STATUS: STATUS_OK, P_KMINE: kr[comm.rank],
+            P_CHILD: n_global + sum(kr[:comm.rank]), P_T: int(keys[last]), P_G: int(g[last])}
+    for k, v in vals.items():
+        plan[k] = v
+    _lib.check(ops.L.igs_shard_mask(gidx.data_ptr(), ops.n, plan.data_ptr(), ops.mask.data_ptr(),
+                                    ops.ws.data_ptr(), ops.ws.numel(), _lib.stream_handle()),
+               "densify_step_sharded")
+    return ops.mask, plan
+
+
+def _resolve_overflow(ops, hist, take_cap, comm, gidx, n_global, scene, beta, maxb):
+    """Re-run the boundary round with room for the largest boundary bucket."""
+    if maxb * comm.world <= MAX_ENTRIES:
+        cap = max(default_record_cap(comm.world), 1 << math.ceil(math.log2(max(maxb, 1))))
+        cap = min(cap, MAX_ENTRIES // comm.world)
+        return _rerun(ops, hist, take_cap, comm, gidx, n_global, scene, beta, cap)
+    rec = ops.boundary(hist, take_cap, gidx, scene, beta, maxb)
+    recs = comm.all_gather(rec)
+    if hasattr(ops, "final_large"):      # the CPU test double
+        return ops.final_large(recs, comm, maxb, n_global, gidx)
+    return _final_large(ops, recs, comm, maxb, n_global, gidx)
 
 
 # ------------------------------------------------------------------ global bookkeeping
@@ -286,14 +357,14 @@ def select_candidates_sharded(stats: DensifyStats, cfg: DensifyConfig, step: int
         gidx = torch.arange(lo, lo + n, dtype=torch.int64, device=dev)
     ops = ops or CudaShardOps(n, dev)
     beta = cfg.split_constants.device_constants()[3]
-    cap = record_cap or DEFAULT_RECORD_CAP
+    cap = record_cap or default_record_cap(comm.world)
     hist, (mask, plan) = _protocol(ops, stats, cfg, step, take_cap, comm, gidx, global_count,
                                    scene, beta, cap)
     pinned = _las.pinned_summary(dev, PLAN_WORDS) if dev.type == "cuda" else _host_buf()
     p = _read(plan, pinned)
     while p[P_STATUS] == STATUS_OVERFLOW:
-        cap = _overflow_cap(p[P_MAXB])
-        mask, plan = _rerun(ops, hist, take_cap, comm, gidx, global_count, scene, beta, cap)
+        mask, plan = _resolve_overflow(ops, hist, take_cap, comm, gidx, global_count, scene, beta,
+                                       p[P_MAXB])
         p = _read(plan, pinned)
     return (mask.view(torch.bool), p) if return_plan else mask.view(torch.bool)
 
@@ -317,11 +388,11 @@ def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: i
     take_cap = _take_cap_global(cfg, glob)
     n = scene.count
     _reserve(scene, n + min(take_cap, n))
-    ops = select_ops or CudaShardOps(n, stats._device)
+    ops = select_ops or CudaShardOps.cached(scene, n, stats._device)
     c = cfg.split_constants
     alpha, log_alpha, log_gamma, beta = c.device_constants()
     gidx = scene._gidx
-    cap = DEFAULT_RECORD_CAP
+    cap = default_record_cap(comm.world)
     pinned = _las.pinned_summary(scene.device, PLAN_WORDS)
     hist, (mask, plan) = _protocol(ops, stats, cfg, step, take_cap, comm, gidx, glob.count,
                                    scene, beta, cap)
@@ -334,8 +405,8 @@ def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: i
         p = _read(plan, pinned)                                    # the event's one host read
         if p[P_STATUS] != STATUS_OVERFLOW:
             break
-        cap = _overflow_cap(p[P_MAXB])                             # nothing was written
-        mask, plan = _rerun(ops, hist, take_cap, comm, gidx, glob.count, scene, beta, cap)
+        mask, plan = _resolve_overflow(ops, hist, take_cap, comm, gidx, glob.count, scene,
+                                       beta, p[P_MAXB])            # nothing was written
     split = p[P_TAKE] if p[P_STATUS] == STATUS_OK else 0
     if split and p[P_FLAGS] & _lib.IGS_LAS_BAD_OPACITY:
         raise ValueError("logit requires all values strictly inside (0, 1)")

@@ -81,6 +81,9 @@ class NumpyShardOps:
             rec[S.REC_HDR + 1:S.REC_HDR + 2 * m:2] = gi[sel[:m]]
         return torch.from_numpy(rec)
 
+    def final_large(self, records, comm, cap, n_global, gidx):
+        return self.finalize(records, comm.rank, cap, n_global, gidx)
+
     def finalize(self, records, rank, cap, n_global, gidx):
         recs = records.cpu().numpy().reshape(records.shape[0], -1)
         plan = np.zeros(S.PLAN_WORDS, np.int64)

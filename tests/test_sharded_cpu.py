@@ -100,6 +100,8 @@ for _n, _tied in ((1001, False), (4000, True), (17, True)):
 CASES.append((np.full(999, 3e-4), np.full(999, 0.5), 2000, "product", 0.5, 999, None))
 CASES.append((np.full(999, 3e-4), np.full(999, 0.5), 2000, "product", 0.5, 999, 16))
 CASES.append((np.full(50, 1e-6), np.full(50, 0.5), 2000, "product", 0.5, 50, None))
+# a boundary bucket beyond the kernel's selection capacity (the device-sort path)
+CASES.append((np.full(9000, 3e-4), np.full(9000, 0.5), 2000, "product", 0.4, 9000, None))
 # scores outside the digit's fine range, negatives, zeros
 _g = _rng.exponential(2e-4, 600)
 _e = np.concatenate([np.full(100, 1e30), np.full(100, -2.0), np.zeros(100), _rng.random(300)])

@@ -48,6 +48,24 @@ def test_world1_sharded_select_equals_single(n, tied):
         np.testing.assert_array_equal(single, want)
 
 
+@pytest.mark.parametrize("n,world_cap", [(20_000, None), (3_000, 8)])
+def test_world1_degenerate_boundary_bucket(n, world_cap):
+    """Every score equal (a warm-up event with all edge scores 0): the whole eligible set is
+    one boundary bucket -- larger than the kernel's selection capacity (device-sort path), or
+    than a small record (re-run path); ties break by index as the stable argsort does."""
+    import paper_2603_08661_b200 as b
+    from paper_2603_08661_b200 import sharded
+    grad, edge = np.full(n, 3e-4), np.zeros(n)
+    for step in (500, 2000):
+        cfg = b.DensifyConfig(budget=10 * n, growth_cap=0.3)
+        st = _stats(b, grad, 1, edge)
+        got = sharded.select_candidates_sharded(st, cfg, step, n, n,
+                                                record_cap=world_cap).cpu().numpy()
+        warm = OS.is_warmup_step(500, 15000, 500, 3, step)
+        want, _ = OS.select_candidates(grad, edge, warm, "product", 2e-4, 0.3, n)
+        np.testing.assert_array_equal(got, want)
+
+
 def test_world1_order_semantics():
     import paper_2603_08661_b200 as b
     from paper_2603_08661_b200 import sharded
