@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "igs_common.cuh"
 
@@ -40,7 +41,7 @@ static_assert(SUBS <= 32, "one warp scans the tile");
 constexpr int MAX_CTAS = 2048;  // fused split: per-CTA totals / flags (grid <= 8 x SMs)
 
 struct Layout {
-  size_t tile_cnt, tile_off, cta_tot, cta_flag, guard, total;
+  size_t tile_cnt, tile_off, cta_tot, cta_flag, guard, list, total;
 };
 
 Layout layout(long long count) {
@@ -51,7 +52,8 @@ Layout layout(long long count) {
   L.cta_tot = L.tile_off + align_up(sizeof(unsigned long long) * (size_t)(tiles + 1), 256);
   L.cta_flag = L.cta_tot + sizeof(unsigned long long) * MAX_CTAS;
   L.guard = L.cta_flag + sizeof(unsigned) * MAX_CTAS;  // the summary's device copy
-  L.total = L.guard + 2 * sizeof(unsigned long long);
+  L.list = align_up(L.guard + 2 * sizeof(unsigned long long), 256);  // list-mode parents
+  L.total = L.list + align_up(sizeof(unsigned) * (size_t)count, 256);
   return L;
 }
 
@@ -91,7 +93,7 @@ __device__ __forceinline__ unsigned prepare_tile(const uint8_t* __restrict__ mas
 #pragma unroll
   for (int j = 0; j < PER; ++j) {  // every load first, then the checks
     const long long i = base + j * NT + threadIdx.x;
-    if (m[j]) {
+    if (m[j] && opac) {  // opac NULL: counts only (the caller has the flags)
       if (rot) q[j] = reinterpret_cast<const float4*>(rot)[i];
       o[j] = opac[i];
     }
@@ -100,6 +102,7 @@ __device__ __forceinline__ unsigned prepare_tile(const uint8_t* __restrict__ mas
   for (int j = 0; j < PER; ++j) {
     if (!m[j]) continue;
     ++local;
+    if (!opac) continue;
     if (rot) {  // 3-D scenes: quaternion checks (2-D scenes pass rot = nullptr)
       float n = quat_norm(q[j]);
       if (!isfinite(n) || n == 0.0f) flags |= IGS_LAS_BAD_QUAT;
@@ -177,6 +180,70 @@ struct Consts {
   float alpha, log_alpha, log_gamma, beta;
 };
 
+// The split of one parent i (las_split.py:78-99 + core.py:32-58 column l): the +offset child
+// in place, the -offset child at row dst (its rotation cloned; SH is cloned by the caller).
+__device__ __forceinline__ void split_parent3(float* __restrict__ pos, float* __restrict__ ls,
+                                              float* __restrict__ rot, float* __restrict__ opac,
+                                              long long i, long long dst, const float (&lv)[3],
+                                              const float (&pv)[3], float ov, float4 qv,
+                                              const Consts& c, int renorm) {
+  // _split_common (las_split.py:78-99)
+  const float l0 = lv[0], l1 = lv[1], l2 = lv[2];
+  int l = 0;  // np.argmax: first maximum (a NaN counts as the maximum)
+  float best = l0;
+  if (!(best != best)) {
+    if (l1 > best || l1 != l1) { l = 1; best = l1; }
+    if (!(best != best) && (l2 > best || l2 != l2)) { l = 2; best = l2; }
+  }
+  const float offset = expf(best) * c.alpha;
+  float cl0 = l0 + c.log_gamma, cl1 = l1 + c.log_gamma, cl2 = l2 + c.log_gamma;
+  const float cll = best + c.log_alpha;
+  if (l == 0) cl0 = cll; else if (l == 1) cl1 = cll; else cl2 = cll;
+  const float raw = raw_opacity(ov, c.beta);
+  const float co = logf(raw / (1.0f - raw));
+
+  // quat_to_rotmat (core.py:32-58), column l only (axis_displacement, las_split.py:62-75)
+  const float4 q = qv;
+  float w = q.x, x = q.y, y = q.z, z = q.w;
+  if (renorm) {
+    float n = quat_norm(q);
+    w = w / n; x = x / n; y = y / n; z = z / n;
+  }
+  float c0, c1, c2;
+  if (l == 0) {
+    c0 = 1.0f - 2.0f * (y * y + z * z);
+    c1 = 2.0f * (x * y + w * z);
+    c2 = 2.0f * (x * z - w * y);
+  } else if (l == 1) {
+    c0 = 2.0f * (x * y - w * z);
+    c1 = 1.0f - 2.0f * (x * x + z * z);
+    c2 = 2.0f * (y * z + w * x);
+  } else {
+    c0 = 2.0f * (x * z + w * y);
+    c1 = 2.0f * (y * z - w * x);
+    c2 = 1.0f - 2.0f * (x * x + y * y);
+  }
+  const float d0 = c0 * offset, d1 = c1 * offset, d2 = c2 * offset;
+  const float p0 = pv[0], p1 = pv[1], p2 = pv[2];
+  // parent slot <- +offset child
+  pos[3 * i] = p0 + d0;
+  pos[3 * i + 1] = p1 + d1;
+  pos[3 * i + 2] = p2 + d2;
+  ls[3 * i] = cl0;
+  ls[3 * i + 1] = cl1;
+  ls[3 * i + 2] = cl2;
+  opac[i] = co;
+  // appended slot <- -offset child
+  pos[3 * dst] = p0 - d0;
+  pos[3 * dst + 1] = p1 - d1;
+  pos[3 * dst + 2] = p2 - d2;
+  ls[3 * dst] = cl0;
+  ls[3 * dst + 1] = cl1;
+  ls[3 * dst + 2] = cl2;
+  opac[dst] = co;
+  reinterpret_cast<float4*>(rot)[dst] = q;
+}
+
 struct TileSmem {
   unsigned warp_cnt[SUBS];
   unsigned warp_pre[SUBS];
@@ -246,62 +313,7 @@ __device__ __forceinline__ void apply_tile3(float* __restrict__ pos, float* __re
     const long long dst = (long long)(slot0 + r);
     src_idx[r] = i;
 
-    // _split_common (las_split.py:78-99)
-    const float l0 = lv[j][0], l1 = lv[j][1], l2 = lv[j][2];
-    int l = 0;  // np.argmax: first maximum (a NaN counts as the maximum)
-    float best = l0;
-    if (!(best != best)) {
-      if (l1 > best || l1 != l1) { l = 1; best = l1; }
-      if (!(best != best) && (l2 > best || l2 != l2)) { l = 2; best = l2; }
-    }
-    const float offset = expf(best) * c.alpha;
-    float cl0 = l0 + c.log_gamma, cl1 = l1 + c.log_gamma, cl2 = l2 + c.log_gamma;
-    const float cll = best + c.log_alpha;
-    if (l == 0) cl0 = cll; else if (l == 1) cl1 = cll; else cl2 = cll;
-    const float raw = raw_opacity(ov[j], c.beta);
-    const float co = logf(raw / (1.0f - raw));
-
-    // quat_to_rotmat (core.py:32-58), column l only (axis_displacement, las_split.py:62-75)
-    const float4 q = qv[j];
-    float w = q.x, x = q.y, y = q.z, z = q.w;
-    if (renorm) {
-      float n = quat_norm(q);
-      w = w / n; x = x / n; y = y / n; z = z / n;
-    }
-    float c0, c1, c2;
-    if (l == 0) {
-      c0 = 1.0f - 2.0f * (y * y + z * z);
-      c1 = 2.0f * (x * y + w * z);
-      c2 = 2.0f * (x * z - w * y);
-    } else if (l == 1) {
-      c0 = 2.0f * (x * y - w * z);
-      c1 = 1.0f - 2.0f * (x * x + z * z);
-      c2 = 2.0f * (y * z + w * x);
-    } else {
-      c0 = 2.0f * (x * z + w * y);
-      c1 = 2.0f * (y * z - w * x);
-      c2 = 1.0f - 2.0f * (x * x + y * y);
-    }
-    const float d0 = c0 * offset, d1 = c1 * offset, d2 = c2 * offset;
-    const float p0 = pv[j][0], p1 = pv[j][1], p2 = pv[j][2];
-
-    // parent slot <- +offset child
-    pos[3 * i] = p0 + d0;
-    pos[3 * i + 1] = p1 + d1;
-    pos[3 * i + 2] = p2 + d2;
-    ls[3 * i] = cl0;
-    ls[3 * i + 1] = cl1;
-    ls[3 * i + 2] = cl2;
-    opac[i] = co;
-    // appended slot <- -offset child
-    pos[3 * dst] = p0 - d0;
-    pos[3 * dst + 1] = p1 - d1;
-    pos[3 * dst + 2] = p2 - d2;
-    ls[3 * dst] = cl0;
-    ls[3 * dst + 1] = cl1;
-    ls[3 * dst + 2] = cl2;
-    opac[dst] = co;
-    reinterpret_cast<float4*>(rot)[dst] = q;
+    split_parent3(pos, ls, rot, opac, i, dst, lv[j], pv[j], ov[j], qv[j], c, renorm);
   }
   __syncthreads();
 
@@ -475,7 +487,7 @@ __global__ void __launch_bounds__(NT) las_prepare_coop_kernel(
     const uint8_t* __restrict__ mask, const float* __restrict__ rot,
     const float* __restrict__ opac, long long count, float beta, long long tiles,
     unsigned* tile_cnt, unsigned long long* tile_off, unsigned long long* cta_tot,
-    unsigned* cta_flag, unsigned long long* guard, int64_t* summary) {
+    unsigned* cta_flag, unsigned long long* guard, int64_t* summary, unsigned* list) {
   __shared__ unsigned warp_cnt[NT / 32];
   __shared__ unsigned red[NT / 32];
   __shared__ unsigned long long s_pre, s_tot;
@@ -540,13 +552,114 @@ __global__ void __launch_bounds__(NT) las_prepare_coop_kernel(
       summary[1] = (int64_t)s_flags;
     }
   }
+  if (!list) return;
+  // list mode: the masked parents of this CTA's tiles, in index order, at their slots
+  __syncthreads();
+  __shared__ unsigned wpre[SUBS];
+  for (long long t = t0; t < t1; ++t) {
+    const unsigned long long off = __ldcg(&tile_off[t]);
+    const long long base = t * TILE;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    bool m[PER];
+    unsigned wrank[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const long long i = base + j * NT + threadIdx.x;
+      m[j] = i < count && mask[i];
+      const unsigned bal = __ballot_sync(0xffffffffu, m[j]);
+      wrank[j] = __popc(bal & lanemask_lt());
+      if (lane == 0) wpre[j * (NT / 32) + warp] = __popc(bal);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const unsigned v = threadIdx.x < (unsigned)SUBS ? wpre[threadIdx.x] : 0u;
+      unsigned x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (threadIdx.x >= (unsigned)o) x += y;
+      }
+      if (threadIdx.x < (unsigned)SUBS) wpre[threadIdx.x] = x - v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      if (m[j]) list[off + wpre[j * (NT / 32) + warp] + wrank[j]] = (unsigned)(base + j * NT + threadIdx.x);
+    __syncthreads();
+  }
+}
+
+// List-mode split (sparse masks): persistent blocks walk the compacted parent list in chunks
+// of NT; child j of the list goes to row count + j (ascending parent order, as the tile
+// mode).  Coalesced list reads, one gather per parent record, the chunk's SH rows cloned with
+// cooperative 16-byte copies.  Guarded by {n_split, flags} like las_apply_kernel.
+template <int CLONE_U>
+__global__ void __launch_bounds__(NT, 4) las_apply_list_kernel(
+    float* __restrict__ pos, float* __restrict__ ls, float* __restrict__ rot,
+    float* __restrict__ opac, float* __restrict__ sh, long long sh_floats, long long count,
+    const unsigned* __restrict__ list, Consts c, const unsigned long long* guard,
+    long long capacity) {
+  __shared__ long long src[NT];
+  if (!split_guard(guard, count, capacity, IGS_LAS_BAD_QUAT | IGS_LAS_BAD_OPACITY)) return;
+  const int renorm = (guard[1] & IGS_LAS_RENORM) != 0;
+  const long long ns = (long long)guard[0];
+  for (long long b0 = (long long)blockIdx.x * NT; b0 < ns; b0 += (long long)gridDim.x * NT) {
+    const long long j = b0 + threadIdx.x;
+    const bool v = j < ns;
+    const long long i = v ? (long long)list[j] : 0;
+    float lv[3], pv[3], ov = 0.0f;
+    float4 qv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (v) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        lv[k] = ls[3 * i + k];
+        pv[k] = pos[3 * i + k];
+      }
+      ov = opac[i];
+      qv = reinterpret_cast<const float4*>(rot)[i];
+      split_parent3(pos, ls, rot, opac, i, count + j, lv, pv, ov, qv, c, renorm);
+    }
+    src[threadIdx.x] = i;
+    __syncthreads();
+    const unsigned n = (unsigned)min((long long)NT, ns - b0);
+    const unsigned long long slot0 = (unsigned long long)(count + b0);
+    if (sh_floats == 48) clone_rows<12, CLONE_U>(sh, src, n, slot0);
+    else if (sh_floats == 12) clone_rows<3, CLONE_U>(sh, src, n, slot0);
+    else if ((sh_floats & 3) == 0) {
+      const long long q4 = sh_floats >> 2;
+      const float4* s4 = reinterpret_cast<const float4*>(sh);
+      float4* d4 = reinterpret_cast<float4*>(sh);
+      for (long long e = threadIdx.x; e < (long long)n * q4; e += NT) {
+        const long long k = e / q4, qq = e - k * q4;
+        __stcs(d4 + (long long)(slot0 + k) * q4 + qq, ld_stream_f4(s4 + src[k] * q4 + qq));
+      }
+    } else {
+      for (long long e = threadIdx.x; e < (long long)n * sh_floats; e += NT) {
+        const long long k = e / sh_floats, qq = e - k * sh_floats;
+        sh[(long long)(slot0 + k) * sh_floats + qq] = sh[src[k] * sh_floats + qq];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+inline int list_grid() {
+  static int g = 0;
+  if (!g) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, las_apply_list_kernel<4>, NT, 0) !=
+        cudaSuccess || n < 1)
+      n = 1;
+    g = n * (sm_count() > 0 ? sm_count() : 148);
+  }
+  return g;
 }
 
 template <bool D3>
 int launch_prepare_coop(const uint8_t* mask, const float* rot, const float* opac, long long count,
                         float beta, void* workspace, size_t workspace_bytes, int64_t* summary,
                         cudaStream_t s, const unsigned long long** guard_out,
-                        const unsigned long long** tile_off_out) {
+                        const unsigned long long** tile_off_out, bool want_list = false) {
   Layout L = layout(count);
   if (!workspace || workspace_bytes < L.total) return IGS_ERR_WORKSPACE;
   char* w = (char*)workspace;
@@ -567,8 +680,9 @@ int launch_prepare_coop(const uint8_t* mask, const float* rot, const float* opac
   unsigned long long* cta_tot = (unsigned long long*)(w + L.cta_tot);
   unsigned* cta_flag = (unsigned*)(w + L.cta_flag);
   unsigned long long* guard = (unsigned long long*)(w + L.guard);
+  unsigned* list = want_list ? (unsigned*)(w + L.list) : nullptr;
   void* args[] = {&mask, &rot, &opac, &count, &beta, (void*)&tiles, &tile_cnt, &tile_off,
-                  &cta_tot, &cta_flag, &guard, &summary};
+                  &cta_tot, &cta_flag, &guard, &summary, &list};
   IGS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)las_prepare_coop_kernel<D3>,
                                            dim3((unsigned)grid), dim3(NT), args, 0, s));
   *guard_out = guard;
@@ -668,14 +782,22 @@ int igs_las_split(float* positions, float* log_scales, float* rotations, float* 
     return IGS_OK;
   }
   const unsigned long long *guard = nullptr, *tile_off = nullptr;
+  static const int list_mode = getenv("IGS_LAS_LIST") ? atoi(getenv("IGS_LAS_LIST")) : 0;
   int st = las::launch_prepare_coop<true>(mask, rotations, opacity_logits, count, beta, workspace,
-                                          workspace_bytes, summary, s, &guard, &tile_off);
+                                          workspace_bytes, summary, s, &guard, &tile_off,
+                                          list_mode != 0);
   if (st != IGS_OK) return st;
   const long long tiles = (count + las::TILE - 1) / las::TILE;
   las::Consts c{alpha, log_alpha, log_gamma, beta};
-  las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
-      positions, log_scales, rotations, opacity_logits, sh, sh_floats, count, mask, c, 0,
-      tile_off, guard, capacity);
+  las::Layout L = las::layout(count);
+  if (list_mode)
+    las::las_apply_list_kernel<4><<<las::list_grid(), las::NT, 0, s>>>(
+        positions, log_scales, rotations, opacity_logits, sh, sh_floats, count,
+        (const unsigned*)((char*)workspace + L.list), c, guard, capacity);
+  else
+    las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
+        positions, log_scales, rotations, opacity_logits, sh, sh_floats, count, mask, c, 0,
+        tile_off, guard, capacity);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }
@@ -728,8 +850,9 @@ int igs_las_split_guarded(float* positions, float* log_scales, float* rotations,
   int64_t* local_summary = (int64_t*)((char*)workspace + L.guard);
   const unsigned long long *local_guard = nullptr, *tile_off = nullptr;
   const int st = dims == 3
-      ? las::launch_prepare_coop<true>(mask, rotations, opacity_logits, count, beta, workspace,
-                                       workspace_bytes, local_summary, s, &local_guard, &tile_off)
+      ? las::launch_prepare_coop<true>(mask, nullptr, nullptr, count, beta, workspace,
+                                       workspace_bytes, local_summary, s, &local_guard, &tile_off,
+                                       true)  // counts and the parent list: the flags are in guard
       : las::launch_prepare_coop<false>(mask, nullptr, opacity_logits, count, beta, workspace,
                                         workspace_bytes, local_summary, s, &local_guard,
                                         &tile_off);
@@ -737,9 +860,10 @@ int igs_las_split_guarded(float* positions, float* log_scales, float* rotations,
   const long long tiles = (count + las::TILE - 1) / las::TILE;
   las::Consts c{alpha, log_alpha, log_gamma, beta};
   if (dims == 3)
-    las::las_apply_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
-        positions, log_scales, rotations, opacity_logits, sh_or_colors, sh_floats, count, mask,
-        c, 0, tile_off, (const unsigned long long*)guard, reserved_rows);
+    las::las_apply_list_kernel<4><<<las::list_grid(), las::NT, 0, s>>>(
+        positions, log_scales, rotations, opacity_logits, sh_or_colors, sh_floats, count,
+        (const unsigned*)((char*)workspace + L.list), c, (const unsigned long long*)guard,
+        reserved_rows);
   else
     las::las2d_apply_kernel<<<(unsigned)tiles, las::NT, 0, s>>>(
         positions, log_scales, rotations, opacity_logits, sh_or_colors, count, mask, c, tile_off,

@@ -240,7 +240,9 @@ __device__ __forceinline__ unsigned las_flags(const float* rot, const float* opa
   return f;
 }
 
-__global__ void __launch_bounds__(NT) compact_kernel(const unsigned long long* __restrict__ keys,
+constexpr int NTC = 256;  // compact_kernel block
+
+__global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* __restrict__ keys,
                                                      const long long* __restrict__ gidx,
                                                      const float* rot, const float* opac,
                                                      float beta, long long n, const State* st,
@@ -256,25 +258,43 @@ __global__ void __launch_bounds__(NT) compact_kernel(const unsigned long long* _
   long long lo, hi;
   block_range(n, lo, hi);
   unsigned lt = 0, fl = 0;
-  for (long long i0 = lo + threadIdx.x; i0 < hi; i0 += U * NT) {
+  // the loop runs the same trip count in every lane, so the warp-aggregated appends below see
+  // every lane (inactive lanes carry kIneligible)
+  const long long span = hi - lo;
+  const long long trips = (span + (long long)U * NTC - 1) / ((long long)U * NTC);
+  const unsigned lanelt = lanemask_lt();
+  for (long long it = 0; it < trips; ++it) {
+    const long long i0 = lo + it * U * NTC + threadIdx.x;
     unsigned long long kv[U];
+    int dv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) kv[u] = i0 + u * NT < hi ? keys[i0 + u * NT] : kIneligible;
+    for (int u = 0; u < U; ++u) kv[u] = i0 + u * NTC < hi ? keys[i0 + u * NTC] : kIneligible;
+#pragma unroll
+    for (int u = 0; u < U; ++u) dv[u] = kv[u] == kIneligible ? NBINS : key_digit(kv[u]);
+    unsigned fu[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)  // the selected and boundary rows' LAS flags (loads in flight)
+      fu[u] = dv[u] <= B ? las_flags(rot, opac, i0 + u * NTC, beta) : 0u;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (kv[u] == kIneligible) continue;
-      const long long i = i0 + u * NT;
-      const int d = key_digit(kv[u]);
-      if (d < B) {
+      if (dv[u] < B) {
         ++lt;
-        fl |= las_flags(rot, opac, i, beta);
-      } else if (d == B) {
-        const unsigned long long f = las_flags(rot, opac, i, beta);
-        const unsigned long long slot =
-            (unsigned long long)atomicAdd((unsigned long long*)&record[R_BCNT], 1ull);
+        fl |= fu[u];
+      }
+      const bool bnd = dv[u] == B;
+      const unsigned bal = __ballot_sync(0xffffffffu, bnd);
+      if (!bal) continue;
+      unsigned long long base = 0;
+      if ((threadIdx.x & 31) == 0)  // one append per warp
+        base = atomicAdd((unsigned long long*)&record[R_BCNT], (unsigned long long)__popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (bnd) {
+        const unsigned long long slot = base + __popc(bal & lanelt);
         if ((long long)slot < cap) {
+          const long long i = i0 + u * NTC;
           record[R_HDR + 2 * slot] = (long long)kv[u];
-          record[R_HDR + 2 * slot + 1] = (long long)((unsigned long long)gidx[i] | (f << 56));
+          record[R_HDR + 2 * slot + 1] =
+              (long long)((unsigned long long)gidx[i] | ((unsigned long long)fu[u] << 56));
         }
       }
     }
@@ -584,11 +604,11 @@ int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64
   shard::resolve_kernel<<<1, shard::NT, 0, st>>>(global_hist, take_cap, S, (long long*)record);
   IGS_LAUNCH_CHECK();
   if (n == 0) return IGS_OK;
-  long long cgrid = (n + shard::NT * shard::U - 1) / (shard::NT * shard::U);
-  const long long cmax = 2LL * (sm_count() > 0 ? sm_count() : 148);
+  long long cgrid = (n + shard::NTC * shard::U - 1) / (shard::NTC * shard::U);
+  const long long cmax = 8LL * (sm_count() > 0 ? sm_count() : 148);
   if (cgrid > cmax) cgrid = cmax;
   if (cgrid < 1) cgrid = 1;
-  shard::compact_kernel<<<(unsigned)cgrid, shard::NT, 0, st>>>(
+  shard::compact_kernel<<<(unsigned)cgrid, shard::NTC, 0, st>>>(
       (const unsigned long long*)(w + L.keys), (const long long*)gidx, rotations, opacity_logits,
       beta, n, S, record_cap, (long long*)record);
   IGS_LAUNCH_CHECK();

@@ -8,7 +8,8 @@ import paper_2603_08661_b200 as igs
 from paper_2603_08661_b200 import sharded
 from paper_2603_08661_b200.synth import random_cloud, synth_view
 
-views = np.stack([synth_view(70, 150, 7000 + k) for k in range(3)])
+# 20 views: the 16-slot candidate / survivor ring wraps (views 16..19 reuse slots 0..3)
+views = np.stack([synth_view(70, 150, 7000 + k) for k in range(20)])
 igs.importance_batch(torch.from_numpy(views).cuda())
 igs.importance_batch(torch.from_numpy(views[:, :, :, 0].copy()).cuda(), median=False)
 igs.importance_pipeline(views[0], nms=False)
@@ -28,6 +29,9 @@ st2._grad_sum.copy_(torch.from_numpy(np.random.default_rng(4).exponential(3e-4, 
 st2._accum_count = 1
 st2.set_edge_score(np.random.default_rng(5).random(n))
 print(int(sharded.select_candidates_sharded(st2, cfg, 2000, n, n).sum()))
+# the sharded densify step at world 1 (keys / boundary / finalize / list-mode split / child index)
+scene_s = igs.Scene3(pos, ls, q, o, sh, capacity=2 * n)
+print(sharded.densify_step_sharded(scene_s, st2, cfg, 2000))
 # fused 2-D split through densify_step, a fused split that must not write (budget), scene IO
 m = 500
 sc2 = igs.Scene2(np.random.default_rng(6).normal(size=(m, 2)), np.zeros((m, 2)), np.zeros(m),
