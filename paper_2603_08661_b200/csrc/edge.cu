@@ -518,6 +518,7 @@ __device__ __forceinline__ double mag_exact(const Params& p, const Smem& s, int 
 // w + NWARP, lane l columns l + 32 k.  Suppressed pixels store 0 here; survivors and
 // undecided pixels are appended to s.list as (r << 12) | (c << 2) | (undecided prev << 1) |
 // undecided next (warp-aggregated).
+template <bool NMS, bool MED>
 __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw, int cb,
                                 int y_first, int cnt, int parity, unsigned long long pol_mid) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -539,7 +540,7 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
       entry[hh][k] = 0;
       if (row_ok) {
         const unsigned qc = qrow[c];
-        if (p.nms) {
+        if (NMS) {
           const int bn = (int)(qc & 3u);
           // prev (dy, dx): bin0 (0,-1), bin1 (-1,-1), bin2 (-1,0), bin3 (-1,+1); next = -prev
           const int po = bn == 0 ? -1 : bn - MWP - 2;  // prev as an offset in s.q cells
@@ -560,7 +561,7 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
         need = need && in;
         // every pixel gets a full-line store here (0); survivors are overwritten by finish
         // (no median) or by the apply pass (median), so no line is ever partially written
-        st_hint_if((p.median || !need) && in, orow + c, 0.0, pol_mid);
+        st_hint_if((MED || !need) && in, orow + c, 0.0, pol_mid);
       }
       bal[hh][k] = __ballot_sync(0xffffffffu, need);
       tot[hh] += __popc(bal[hh][k]);
@@ -571,7 +572,7 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
   if (lane == 0) {
     if (tot[0] + tot[1]) {
       lbase0 = atomicAdd(&s.list_n[parity], tot[0] + tot[1]);
-      if (p.median) gbase = atomicAdd(&p.ctl[v].nsurv, tot[0] + tot[1]);
+      if (MED) gbase = atomicAdd(&p.ctl[v].nsurv, tot[0] + tot[1]);
     }
     lbase1 = lbase0 + tot[0];
   }
@@ -586,7 +587,7 @@ __device__ void band_nms_decide(const Params& p, Smem& s, int v, int x0, int xw,
       pre += __popc(bal[hh][k]);
     }
   }
-  if (lane == 0 && p.median) {  // row r's entries: list [rowl, ...) -> survivor list [rowg, ...)
+  if (lane == 0 && MED) {  // row r's entries: list [rowl, ...) -> survivor list [rowg, ...)
     const int r0 = warp, r1 = warp + NWARP;
     if (r0 < cnt) { s.rowl[r0] = lbase0; s.rowg[r0] = gbase; }
     if (r1 < cnt) { s.rowl[r1] = lbase1; s.rowg[r1] = gbase + tot[0]; }
@@ -711,7 +712,13 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
     if (more) shift_rows<double, GWP>(s.g, n, 8);
     __syncthreads();
     PHASE_MARK(2);
-    band_nms_decide(p, s, v, x0, xw, cb, Y, n, parity, pol_mid);
+    if (p.nms) {
+      if (p.median) band_nms_decide<true, true>(p, s, v, x0, xw, cb, Y, n, parity, pol_mid);
+      else band_nms_decide<true, false>(p, s, v, x0, xw, cb, Y, n, parity, pol_mid);
+    } else {
+      if (p.median) band_nms_decide<false, true>(p, s, v, x0, xw, cb, Y, n, parity, pol_mid);
+      else band_nms_decide<false, false>(p, s, v, x0, xw, cb, Y, n, parity, pol_mid);
+    }
     __syncthreads();
     PHASE_MARK(3);
     band_nms_finish(p, s, v, x0, Y, parity, pol_mid);
