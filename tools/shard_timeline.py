@@ -60,3 +60,12 @@ for s, e, name in rows[first:]:
     print(f"+{(s - tot0):8.1f} us  gap {s - prev:7.1f}  dur {e - s:7.1f}  {name}")
     prev = e
 print(f"device span {rows[-1][1] - tot0:.1f} us")
+
+# host-side view of the step: CPU op spans from the same profile
+cpu = [e for e in prof.events() if e.device_type.name == "CPU"]
+cpu.sort(key=lambda e: e.time_range.start)
+t0 = cpu[0].time_range.start if cpu else 0
+for e in cpu:
+    d = e.time_range.end - e.time_range.start
+    if d > 4.0:
+        print(f"cpu +{e.time_range.start - t0:8.1f} us dur {d:7.1f}  {e.name[:70]}")
