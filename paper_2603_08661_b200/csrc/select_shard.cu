@@ -218,13 +218,11 @@ __global__ void __launch_bounds__(NT) resolve_kernel(const int* __restrict__ his
   }
 }
 
-// numpy float32 LAS pre-pass flags of one parent (las.cu prepare_tile).
-__device__ __forceinline__ unsigned las_flags(const float* rot, const float* opac, long long i,
-                                              float beta) {
+// numpy float32 LAS pre-pass flags of one parent (las.cu prepare_tile), from its loaded
+// quaternion (3-D) and opacity logit.
+__device__ __forceinline__ unsigned las_flags_of(bool d3, float4 q, float o, float beta) {
   unsigned f = 0;
-  if (!opac) return 0;  // selection only (no scene): no split flags
-  if (rot) {
-    const float4 q = reinterpret_cast<const float4*>(rot)[i];
+  if (d3) {
     float s = q.x * q.x;
     s = s + q.y * q.y;
     s = s + q.z * q.z;
@@ -233,7 +231,7 @@ __device__ __forceinline__ unsigned las_flags(const float* rot, const float* opa
     if (!isfinite(nrm) || nrm == 0.0f) f |= IGS_LAS_BAD_QUAT;
     else if (fabsf(nrm - 1.0f) > 1e-4f) f |= IGS_LAS_RENORM;
   }
-  const float e = expf(-opac[i]);
+  const float e = expf(-o);
   const float sg = 1.0f / (1.0f + e);
   const float r = sg * beta;
   if (!(r > 0.0f && r < 1.0f)) f |= IGS_LAS_BAD_OPACITY;
@@ -241,6 +239,7 @@ __device__ __forceinline__ unsigned las_flags(const float* rot, const float* opa
 }
 
 constexpr int NTC = 256;  // compact_kernel block
+constexpr int UC = 8;     // compact_kernel keys per thread per step
 
 __global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* __restrict__ keys,
                                                      const long long* __restrict__ gidx,
@@ -261,25 +260,35 @@ __global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* 
   // the loop runs the same trip count in every lane, so the warp-aggregated appends below see
   // every lane (inactive lanes carry kIneligible)
   const long long span = hi - lo;
-  const long long trips = (span + (long long)U * NTC - 1) / ((long long)U * NTC);
+  const long long trips = (span + (long long)UC * NTC - 1) / ((long long)UC * NTC);
   const unsigned lanelt = lanemask_lt();
   for (long long it = 0; it < trips; ++it) {
-    const long long i0 = lo + it * U * NTC + threadIdx.x;
-    unsigned long long kv[U];
-    int dv[U];
+    const long long i0 = lo + it * UC * NTC + threadIdx.x;
+    unsigned long long kv[UC];
+    int dv[UC];
 #pragma unroll
-    for (int u = 0; u < U; ++u) kv[u] = i0 + u * NTC < hi ? keys[i0 + u * NTC] : kIneligible;
+    for (int u = 0; u < UC; ++u) kv[u] = i0 + u * NTC < hi ? keys[i0 + u * NTC] : kIneligible;
 #pragma unroll
-    for (int u = 0; u < U; ++u) dv[u] = kv[u] == kIneligible ? NBINS : key_digit(kv[u]);
-    unsigned fu[U];
+    for (int u = 0; u < UC; ++u) dv[u] = kv[u] == kIneligible ? NBINS : key_digit(kv[u]);
+    // the selected and boundary rows' LAS inputs: every load in flight before the arithmetic
+    float4 qv[UC];
+    float ov[UC];
 #pragma unroll
-    for (int u = 0; u < U; ++u)  // the selected and boundary rows' LAS flags (loads in flight)
-      fu[u] = dv[u] <= B ? las_flags(rot, opac, i0 + u * NTC, beta) : 0u;
+    for (int u = 0; u < UC; ++u) {
+      qv[u] = make_float4(1.f, 0.f, 0.f, 0.f);
+      ov[u] = 0.f;
+      if (opac && dv[u] <= B) {
+        const long long i = i0 + u * NTC;
+        if (rot) qv[u] = reinterpret_cast<const float4*>(rot)[i];
+        ov[u] = opac[i];
+      }
+    }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < UC; ++u) {
+      const unsigned fu = (opac && dv[u] <= B) ? las_flags_of(rot != nullptr, qv[u], ov[u], beta) : 0u;
       if (dv[u] < B) {
         ++lt;
-        fl |= fu[u];
+        fl |= fu;
       }
       const bool bnd = dv[u] == B;
       const unsigned bal = __ballot_sync(0xffffffffu, bnd);
@@ -294,7 +303,7 @@ __global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* 
           const long long i = i0 + u * NTC;
           record[R_HDR + 2 * slot] = (long long)kv[u];
           record[R_HDR + 2 * slot + 1] =
-              (long long)((unsigned long long)gidx[i] | ((unsigned long long)fu[u] << 56));
+              (long long)((unsigned long long)gidx[i] | ((unsigned long long)fu << 56));
         }
       }
     }
@@ -604,7 +613,7 @@ int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64
   shard::resolve_kernel<<<1, shard::NT, 0, st>>>(global_hist, take_cap, S, (long long*)record);
   IGS_LAUNCH_CHECK();
   if (n == 0) return IGS_OK;
-  long long cgrid = (n + shard::NTC * shard::U - 1) / (shard::NTC * shard::U);
+  long long cgrid = (n + shard::NTC * shard::UC - 1) / (shard::NTC * shard::UC);
   const long long cmax = 8LL * (sm_count() > 0 ? sm_count() : 148);
   if (cgrid > cmax) cgrid = cmax;
   if (cgrid < 1) cgrid = 1;
