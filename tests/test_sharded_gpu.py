@@ -255,3 +255,28 @@ def test_world1_sharded_select_reference_golden():
         st = _stats(b, c["grad_sum"], int(c["accum"]), c["edge"])
         got = sharded.select_candidates_sharded(st, cfg, int(step), int(headroom), n)
         np.testing.assert_array_equal(got.cpu().numpy(), c["mask"], err_msg=name)
+
+
+@pytest.mark.parametrize("k_sh", [1, 4, 9, 16])
+def test_world1_sharded_step_sh_sizes(k_sh):
+    """The list-mode guarded split of the sharded step for every SH row width (3, 12, 27 and
+    48 floats: scalar, float4 and the unrolled clone paths) against the single-device step."""
+    import paper_2603_08661_b200 as b
+    from paper_2603_08661_b200 import sharded
+    n = 5_003
+    pos, ls, qq, o, sh = _cloud(n, 31)
+    sh = np.ascontiguousarray(np.repeat(sh[:, :1, :], k_sh, axis=1) +
+                              np.arange(k_sh, dtype=np.float32)[None, :, None])
+    rng = np.random.default_rng(32)
+    grad, edge = rng.exponential(3e-4, n), rng.random(n)
+    want = b.Scene3(pos, ls, qq, o, sh, capacity=2 * n)
+    ev_w = b.densify_step(want, _stats(b, grad, 1, edge), b.DensifyConfig(budget=2 * n,
+                                                                          growth_cap=0.2), 2000)
+    got = b.Scene3(pos, ls, qq, o, sh, capacity=2 * n)
+    ev_g = sharded.densify_step_sharded(got, _stats(b, grad, 1, edge),
+                                        b.DensifyConfig(budget=2 * n, growth_cap=0.2), 2000)
+    assert (ev_g.eligible, ev_g.split, ev_g.count_after) == \
+        (ev_w.eligible, ev_w.split, ev_w.count_after)
+    gw, gg = want.to_numpy(), got.to_numpy()
+    for col in ("positions", "log_scales", "rotations", "opacity_logits", "sh"):
+        np.testing.assert_array_equal(gg[col], gw[col], err_msg=col)
