@@ -16,7 +16,7 @@ cat gpurun_out/bench_ref_$TAG.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-uhd --no-check \
   > gpurun_out/ncu_launch_bench_$TAG.json 2>&1
-python tools/launch_table.py gpurun_out/launches_$TAG.csv | head -25
+python tools/launch_table.py gpurun_out/launches_$TAG.csv > gpurun_out/launch_table_$TAG.txt; head -25 gpurun_out/launch_table_$TAG.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:edge_persistent \
   -s 1 -c 1 -o gpurun_out/edge_full_$TAG -f python tools/edge_modes.py > gpurun_out/ncu_edge_$TAG.log 2>&1
 tail -2 gpurun_out/ncu_edge_$TAG.log
