@@ -280,3 +280,26 @@ def test_world1_sharded_step_sh_sizes(k_sh):
     gw, gg = want.to_numpy(), got.to_numpy()
     for col in ("positions", "log_scales", "rotations", "opacity_logits", "sh"):
         np.testing.assert_array_equal(gg[col], gw[col], err_msg=col)
+
+
+def test_world1_sharded_step_2d_scene():
+    """A 2-D scene through the sharded step (flags without quaternions, the guarded 2-D split)
+    against the single-device densify_step."""
+    import paper_2603_08661_b200 as b
+    from paper_2603_08661_b200 import sharded
+    n = 4_001
+    rng = np.random.default_rng(41)
+    cols = (rng.normal(0, 5, (n, 2)), rng.uniform(-1, 1, (n, 2)), rng.uniform(-3, 3, n),
+            rng.normal(0, 1.5, n), rng.random((n, 3)))
+    grad, edge = rng.exponential(3e-4, n), rng.random(n)
+    want = b.Scene2(*cols, capacity=2 * n)
+    ev_w = b.densify_step(want, _stats(b, grad, 1, edge), b.DensifyConfig(budget=2 * n,
+                                                                          growth_cap=0.2), 2000)
+    got = b.Scene2(*cols, capacity=2 * n)
+    ev_g = sharded.densify_step_sharded(got, _stats(b, grad, 1, edge),
+                                        b.DensifyConfig(budget=2 * n, growth_cap=0.2), 2000)
+    assert (ev_g.eligible, ev_g.split, ev_g.count_after) == \
+        (ev_w.eligible, ev_w.split, ev_w.count_after)
+    gw, gg = want.to_numpy(), got.to_numpy()
+    for col in ("positions", "log_scales", "thetas", "opacity_logits", "colors"):
+        np.testing.assert_array_equal(gg[col], gw[col], err_msg=col)
