@@ -210,6 +210,15 @@ int igs_las_split(float* positions, float* log_scales, float* rotations, float* 
                   const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,
                   void* workspace, size_t workspace_bytes, int64_t* summary, void* stream);
 
+/* igs_las_split for sparse masks (e.g. densify_step's top-5% selection): the pre-pass also
+ * lists the masked parents in slot order and the apply pass walks that list (one gather per
+ * parent) instead of every tile of the mask.  Same results, same guard. */
+int igs_las_split_sparse(float* positions, float* log_scales, float* rotations,
+                         float* opacity_logits, float* sh, int64_t sh_floats, int64_t count,
+                         int64_t capacity, const uint8_t* mask, float alpha, float log_alpha,
+                         float log_gamma, float beta, void* workspace, size_t workspace_bytes,
+                         int64_t* summary, void* stream);
+
 /* 2-D Long-Axis-Split (las_split.py:182-197), after igs_las_prepare with rotations = NULL
  * (no quaternion checks).  Columns: positions (cap,2), log_scales (cap,2), thetas (cap,),
  * opacity_logits (cap,), colors (cap,3), float32; the same slot rule as igs_las_apply. */

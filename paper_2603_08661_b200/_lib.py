@@ -62,6 +62,8 @@ SIGNATURES = {
                              _flt, _int, _vp, _sz, _vp]),
     "igs_las_split": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt, _flt,
                              _flt, _vp, _sz, _vp, _vp]),
+    "igs_las_split_sparse": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt,
+                                    _flt, _flt, _vp, _sz, _vp, _vp]),
     "igs_las2d_split": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _flt, _flt, _flt, _flt,
                                _vp, _sz, _vp, _vp]),
     "igs_las2d_apply": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _flt, _flt, _flt, _flt,

@@ -766,10 +766,11 @@ int igs_las2d_apply(float* positions, float* log_scales, float* thetas, float* o
   return IGS_OK;
 }
 
-int igs_las_split(float* positions, float* log_scales, float* rotations, float* opacity_logits,
-                  float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
-                  const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,
-                  void* workspace, size_t workspace_bytes, int64_t* summary, void* stream) {
+static int las_split_impl(float* positions, float* log_scales, float* rotations,
+                          float* opacity_logits, float* sh, int64_t sh_floats, int64_t count,
+                          int64_t capacity, const uint8_t* mask, float alpha, float log_alpha,
+                          float log_gamma, float beta, void* workspace, size_t workspace_bytes,
+                          int64_t* summary, void* stream, bool list_mode) {
   if (count < 0 || capacity < count || sh_floats < 0 || !summary) return IGS_ERR_ARGUMENT;
   if (count > 0 && (!positions || !log_scales || !rotations || !opacity_logits || !mask))
     return IGS_ERR_ARGUMENT;
@@ -782,10 +783,9 @@ int igs_las_split(float* positions, float* log_scales, float* rotations, float* 
     return IGS_OK;
   }
   const unsigned long long *guard = nullptr, *tile_off = nullptr;
-  static const int list_mode = getenv("IGS_LAS_LIST") ? atoi(getenv("IGS_LAS_LIST")) : 0;
   int st = las::launch_prepare_coop<true>(mask, rotations, opacity_logits, count, beta, workspace,
                                           workspace_bytes, summary, s, &guard, &tile_off,
-                                          list_mode != 0);
+                                          list_mode);
   if (st != IGS_OK) return st;
   const long long tiles = (count + las::TILE - 1) / las::TILE;
   las::Consts c{alpha, log_alpha, log_gamma, beta};
@@ -800,6 +800,25 @@ int igs_las_split(float* positions, float* log_scales, float* rotations, float* 
         tile_off, guard, capacity);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
+}
+
+int igs_las_split(float* positions, float* log_scales, float* rotations, float* opacity_logits,
+                  float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
+                  const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,
+                  void* workspace, size_t workspace_bytes, int64_t* summary, void* stream) {
+  return las_split_impl(positions, log_scales, rotations, opacity_logits, sh, sh_floats, count,
+                        capacity, mask, alpha, log_alpha, log_gamma, beta, workspace,
+                        workspace_bytes, summary, stream, false);
+}
+
+int igs_las_split_sparse(float* positions, float* log_scales, float* rotations,
+                         float* opacity_logits, float* sh, int64_t sh_floats, int64_t count,
+                         int64_t capacity, const uint8_t* mask, float alpha, float log_alpha,
+                         float log_gamma, float beta, void* workspace, size_t workspace_bytes,
+                         int64_t* summary, void* stream) {
+  return las_split_impl(positions, log_scales, rotations, opacity_logits, sh, sh_floats, count,
+                        capacity, mask, alpha, log_alpha, log_gamma, beta, workspace,
+                        workspace_bytes, summary, stream, true);
 }
 
 int igs_las2d_split(float* positions, float* log_scales, float* thetas, float* opacity_logits,

@@ -188,7 +188,8 @@ def densify_step(scene, stats: DensifyStats, cfg: DensifyConfig, step: int) -> D
         # counts | split summary, written by the kernels straight into pinned host memory
         res, view = _las.pinned_summary(stats._device, 4)
         mask, _ = _launch_select(stats, cfg, step, take_cap, counts=res[:2])
-        _las.split_async(scene, mask.view(torch.bool), c, summary=res[2:])
+        _las.split_async(scene, mask.view(torch.bool), c, summary=res[2:],
+                         sparse=4 * take_cap <= n)  # at most a quarter masked: list mode
         _las.sync(stats._device)
         eligible, n_split, flags = int(view[0]), int(view[2]), int(view[3])
         _las.finish_split(scene, n_split, flags)

@@ -152,12 +152,13 @@ def _column_ptrs(scene):
     return hit[1]
 
 
-def split_async(scene, mask, c: SplitConstants, summary=None):
+def split_async(scene, mask, c: SplitConstants, summary=None, sparse=False):
     """Launch the fused split (igs_las_split / igs_las2d_split): ONE cooperative launch that
     runs the pre-pass, a grid barrier, and the apply pass guarded on the device by the
     pre-pass totals, with no host round trip in between.  Returns the summary int64[2] =
     {n_split, flags} (written into ``summary`` when given: device memory or pinned host
-    memory), not yet read."""
+    memory), not yet read.  ``sparse``: the caller knows few parents are masked (3-D: the
+    list-mode apply, igs_las_split_sparse)."""
     L = _lib.lib()
     m = _mask_tensor(mask, scene.count, scene.device)
     nbytes = _lib.query_size(L.igs_las_workspace_bytes, scene.count)
@@ -168,10 +169,10 @@ def split_async(scene, mask, c: SplitConstants, summary=None):
     stream = _lib.stream_handle(scene.device)
     if isinstance(scene, Scene3):
         pos, ls, rot, op, sh = _column_ptrs(scene)
-        _lib.check(L.igs_las_split(pos, ls, rot, op, sh, scene._sh.shape[1] * 3, scene.count,
-                                   scene.capacity, m.data_ptr(), alpha, log_alpha, log_gamma,
-                                   beta, ws.data_ptr(), ws.numel(), summary.data_ptr(),
-                                   stream), "las_split_batch")
+        fn = L.igs_las_split_sparse if sparse else L.igs_las_split
+        _lib.check(fn(pos, ls, rot, op, sh, scene._sh.shape[1] * 3, scene.count,
+                      scene.capacity, m.data_ptr(), alpha, log_alpha, log_gamma, beta,
+                      ws.data_ptr(), ws.numel(), summary.data_ptr(), stream), "las_split_batch")
     else:
         cols = scene._cols
         _lib.check(L.igs_las2d_split(cols["positions"].data_ptr(), cols["log_scales"].data_ptr(),

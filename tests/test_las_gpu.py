@@ -77,6 +77,42 @@ def test_sh_degree3_clone_vs_oracle():
         assert_las_close(s.to_numpy(), want, f"p={p}")
 
 
+@pytest.mark.parametrize("sh_coeffs", [1, 16])
+def test_sparse_list_mode_vs_oracle(sh_coeffs):
+    """igs_las_split_sparse (the list-mode apply densify_step uses) gives the tile-mode results
+    for every mask density, and leaves the scene untouched on a capacity overflow."""
+    b = B()
+    from paper_2603_08661_b200 import las_split as LS
+    from paper_2603_08661_b200.synth import random_cloud
+    n = 50_000
+    pos, ls, q, o, sh = random_cloud(n, sh_coeffs, seed=17 + sh_coeffs)
+    rng = np.random.default_rng(sh_coeffs)
+    for p in (0.0, 0.001, 0.05, 0.5, 1.0):
+        mask = rng.random(n) < p
+        d = {"positions": pos, "log_scales": ls, "rotations": q, "opacity_logits": o, "sh": sh,
+             "capacity": 2 * n}
+        want = OL.las_split_batch(d, mask)
+        s = gpu_scene(d)
+        summ = LS.split_async(s, torch.from_numpy(mask).cuda(), b.SplitConstants(), sparse=True)
+        n_split, flags = (int(v) for v in summ.cpu())
+        assert n_split == int(mask.sum()) and flags == 0
+        LS.finish_split(s, n_split, flags)
+        assert_las_close(s.to_numpy(), want, f"p={p}")
+    d = {"positions": pos, "log_scales": ls, "rotations": q, "opacity_logits": o, "sh": sh,
+         "capacity": n + 10}
+    s = gpu_scene(d)
+    before = s.to_numpy()
+    mask = np.zeros(n, bool)
+    mask[::1000] = True                              # 50 splits > 10 free rows
+    summ = LS.split_async(s, torch.from_numpy(mask).cuda(), b.SplitConstants(), sparse=True)
+    with pytest.raises(b.BudgetError):
+        LS.finish_split(s, *(int(v) for v in summ.cpu()))
+    after = s.to_numpy()
+    assert s.count == n
+    for col in before:
+        assert_array_equal(after[col], before[col], err_msg=col)
+
+
 def test_million_all_masked_acceptance_ratios():
     """Acceptance criterion 1 (test_acceptance.py:61-104) on 1M splits, plus oracle parity."""
     b = B()
