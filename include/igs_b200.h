@@ -55,6 +55,10 @@ int igs_abi_version(void);
 /* cudaStreamSynchronize(stream): the host half of a synchronous call whose kernels write
  * their result into pinned host memory (e.g. igs_las_split's summary). */
 int igs_stream_synchronize(void* stream);
+/* Spin until *word (pinned host memory a kernel writes, e.g. igs_las_split's summary[1]) is no
+ * longer `sentinel`.  After timeout_ns the stream is synchronised instead (an asynchronous
+ * kernel fault returns its CUDA error); IGS_ERR_CUDA if the word is still unwritten. */
+int igs_wait_host_word(const int64_t* word, int64_t sentinel, int64_t timeout_ns, void* stream);
 
 /* L2 set-aside for persisting (evict_last) lines: the fused edge kernel keeps the in-flight
  * views' thinned maps evict_last.  Device-wide (cudaLimitPersistingL2CacheSize), clamped to
@@ -209,6 +213,30 @@ int igs_las_split(float* positions, float* log_scales, float* rotations, float* 
                   float* sh, int64_t sh_floats, int64_t count, int64_t capacity,
                   const uint8_t* mask, float alpha, float log_alpha, float log_gamma, float beta,
                   void* workspace, size_t workspace_bytes, int64_t* summary, void* stream);
+
+/* igs_las_split (sparse = 0) / igs_las_split_sparse (sparse != 0) with the arguments in one
+ * struct: for bindings whose per-argument call cost matters at small sizes (one pointer
+ * instead of 17 converted arguments; the Python drop-in keeps one per scene and updates
+ * count / capacity / mask / summary per call). */
+typedef struct IgsLasSplitArgs {
+  float* positions;
+  float* log_scales;
+  float* rotations;
+  float* opacity_logits;
+  float* sh;
+  int64_t sh_floats;
+  int64_t count;
+  int64_t capacity;
+  const uint8_t* mask;
+  float alpha, log_alpha, log_gamma, beta;
+  void* workspace;
+  size_t workspace_bytes;
+  int64_t* summary;
+  void* stream;
+  int32_t sparse;
+  int32_t reserved;
+} IgsLasSplitArgs;
+int igs_las_split_packed(const IgsLasSplitArgs* args);
 
 /* igs_las_split for sparse masks (e.g. densify_step's top-5% selection): the pre-pass also
  * lists the masked parents in slot order and the apply pass walks that list (one gather per

@@ -31,6 +31,7 @@ SIGNATURES = {
     "igs_last_cuda_error": (C.c_char_p, []),
     "igs_abi_version": (_int, []),
     "igs_stream_synchronize": (_int, [_vp]),
+    "igs_wait_host_word": (_int, [_vp, _i64, _i64, _vp]),
     "igs_l2_set_aside": (_int, [_sz, _szp]),
     "igs_edge_workspace_bytes": (_int, [_i64, _i64, _i64, _int, _szp]),
     "igs_edge_importance": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _int, _vp, _vp, _sz,
@@ -62,6 +63,7 @@ SIGNATURES = {
                              _flt, _int, _vp, _sz, _vp]),
     "igs_las_split": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt, _flt,
                              _flt, _vp, _sz, _vp, _vp]),
+    "igs_las_split_packed": (_int, [_vp]),
     "igs_las_split_sparse": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt,
                                     _flt, _flt, _vp, _sz, _vp, _vp]),
     "igs_las2d_split": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _flt, _flt, _flt, _flt,
@@ -123,6 +125,16 @@ try:  # the raw cudaStream_t of the current stream without building a Stream obj
     _raw_stream = torch._C._cuda_getCurrentRawStream
 except AttributeError:  # pragma: no cover - older torch
     _raw_stream = None
+
+
+class LasSplitArgs(C.Structure):
+    """Mirror of IgsLasSplitArgs (include/igs_b200.h)."""
+    _fields_ = [("positions", _vp), ("log_scales", _vp), ("rotations", _vp),
+                ("opacity_logits", _vp), ("sh", _vp), ("sh_floats", _i64), ("count", _i64),
+                ("capacity", _i64), ("mask", _vp), ("alpha", _flt), ("log_alpha", _flt),
+                ("log_gamma", _flt), ("beta", _flt), ("workspace", _vp),
+                ("workspace_bytes", _sz), ("summary", _vp), ("stream", _vp),
+                ("sparse", C.c_int32), ("reserved", C.c_int32)]
 
 
 def stream_handle(device=None) -> int:

@@ -1,5 +1,7 @@
 // C-ABI housekeeping: status strings, CUDA error capture, device queries.
 #include <cuda_runtime.h>
+
+#include <chrono>
 #include <stdio.h>
 
 #include "igs_common.cuh"
@@ -48,6 +50,25 @@ int igs_abi_version(void) { return 1; }
 int igs_stream_synchronize(void* stream) {
   IGS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   return IGS_OK;
+}
+
+// Spin until the host word (pinned memory a kernel writes) differs from `sentinel`; after
+// `timeout_ns` fall back to synchronising `stream` (so an asynchronous kernel fault surfaces
+// as its CUDA error) and fail with IGS_ERR_CUDA if the word is still unwritten.
+int igs_wait_host_word(const int64_t* word, int64_t sentinel, int64_t timeout_ns, void* stream) {
+  if (!word) return IGS_ERR_ARGUMENT;
+  const volatile int64_t* w = word;
+  if (*w != sentinel) return IGS_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 1;; ++spin) {
+    if (*w != sentinel) return IGS_OK;
+    if ((spin & 1023u) == 0 &&
+        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0)
+                .count() > timeout_ns)
+      break;
+  }
+  IGS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return *w != sentinel ? IGS_OK : IGS_ERR_CUDA;
 }
 
 // L2 set-aside for persisting (evict_last) lines on the current device; returns the granted

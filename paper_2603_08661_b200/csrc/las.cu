@@ -548,7 +548,9 @@ __global__ void __launch_bounds__(NT) las_prepare_coop_kernel(
     if (b == 0) {
       guard[0] = s_tot;
       guard[1] = s_flags;
+      // summary[1] last: a host polling it (igs_wait_host_word) then reads a complete summary
       summary[0] = (int64_t)s_tot;
+      __threadfence_system();
       summary[1] = (int64_t)s_flags;
     }
   }
@@ -809,6 +811,14 @@ int igs_las_split(float* positions, float* log_scales, float* rotations, float* 
   return las_split_impl(positions, log_scales, rotations, opacity_logits, sh, sh_floats, count,
                         capacity, mask, alpha, log_alpha, log_gamma, beta, workspace,
                         workspace_bytes, summary, stream, false);
+}
+
+int igs_las_split_packed(const IgsLasSplitArgs* a) {
+  if (!a) return IGS_ERR_ARGUMENT;
+  return las_split_impl(a->positions, a->log_scales, a->rotations, a->opacity_logits, a->sh,
+                        a->sh_floats, a->count, a->capacity, a->mask, a->alpha, a->log_alpha,
+                        a->log_gamma, a->beta, a->workspace, a->workspace_bytes, a->summary,
+                        a->stream, a->sparse != 0);
 }
 
 int igs_las_split_sparse(float* positions, float* log_scales, float* rotations,

@@ -16,6 +16,7 @@ The sharded path keeps the two-call form (``igs_las_prepare`` -> global checks
 
 from __future__ import annotations
 
+import ctypes
 import functools
 import math
 from dataclasses import dataclass
@@ -136,6 +137,17 @@ def pinned_summary(device, n=2):
     return hit
 
 
+_UNSET = -1  # summary[1] (flags, >= 0) before the pre-pass writes it
+
+
+def wait_summary(device, buf):
+    """Wait until the pre-pass has written the pinned summary `buf` (its flags word last):
+    the apply pass may still be running on the stream -- later work on the stream, and any
+    host read of the scene (which synchronises), sees the split scene."""
+    _lib.check(_lib.lib().igs_wait_host_word(buf.data_ptr() + 8, _UNSET, 2_000_000_000,
+                                             _lib.stream_handle(device)), "las_split_batch")
+
+
 def sync(device):
     """Wait for the current stream of `device` (one C call on the raw stream handle)."""
     _lib.check(_lib.lib().igs_stream_synchronize(_lib.stream_handle(device)), "synchronize")
@@ -152,35 +164,95 @@ def _column_ptrs(scene):
     return hit[1]
 
 
-def split_async(scene, mask, c: SplitConstants, summary=None, sparse=False):
-    """Launch the fused split (igs_las_split / igs_las2d_split): ONE cooperative launch that
-    runs the pre-pass, a grid barrier, and the apply pass guarded on the device by the
-    pre-pass totals, with no host round trip in between.  Returns the summary int64[2] =
-    {n_split, flags} (written into ``summary`` when given: device memory or pinned host
-    memory), not yet read.  ``sparse``: the caller knows few parents are masked (3-D: the
-    list-mode apply, igs_las_split_sparse)."""
+class _LasPlan:
+    """Per-scene packed arguments of igs_las_split_packed: rebuilt when a column buffer, the
+    stream or the constants change; count / capacity / mask / summary are set per call."""
+
+    __slots__ = ("bufs", "stream", "consts", "args", "addr", "ws_rows", "ws", "pin")
+
+
+def _plan3(scene, c, stream):
+    p = scene.__dict__.get("_las_plan")
+    if (p is None or p.stream != stream or (p.consts is not c and p.consts != c)
+            or p.bufs[0] is not scene._pos
+            or p.bufs[1] is not scene._ls or p.bufs[2] is not scene._rot
+            or p.bufs[3] is not scene._op or p.bufs[4] is not scene._sh):
+        p = _LasPlan()
+        p.bufs = (scene._pos, scene._ls, scene._rot, scene._op, scene._sh)
+        p.stream, p.consts = stream, c
+        a = _lib.LasSplitArgs()
+        (a.positions, a.log_scales, a.rotations, a.opacity_logits,
+         a.sh) = (b.data_ptr() for b in p.bufs)
+        a.sh_floats = scene._sh.shape[1] * 3
+        a.alpha, a.log_alpha, a.log_gamma, a.beta = c.device_constants()
+        a.stream = stream
+        p.args, p.addr, p.ws_rows, p.ws, p.pin = a, ctypes.addressof(a), -1, None, None
+        scene.__dict__["_las_plan"] = p
+    return p
+
+
+def _split3(scene, mask, c):
+    """las_split_batch on a Scene3: one packed launch call, then a spin on the pinned summary's
+    flags word; the host work around the launch is kept to attribute loads (configs[0] is
+    latency-bound)."""
     L = _lib.lib()
-    m = _mask_tensor(mask, scene.count, scene.device)
-    nbytes = _lib.query_size(L.igs_las_workspace_bytes, scene.count)
-    ws = _lib.workspace(nbytes, scene.device, "las")
+    n = scene._count
+    dev = scene._pos.device
+    m = _mask_tensor(mask, n, dev)
+    stream = _lib.stream_handle(dev)
+    p = _plan3(scene, c, stream)
+    a = p.args
+    if p.ws_rows < n:
+        p.ws = _lib.workspace(_lib.query_size(L.igs_las_workspace_bytes, n), dev, "las")
+        a.workspace, a.workspace_bytes, p.ws_rows = p.ws.data_ptr(), p.ws.numel(), n
+    if p.pin is None:
+        buf, view = pinned_summary(dev)
+        p.pin = (buf, view, buf.data_ptr())
+    _, view, baddr = p.pin
+    view[1] = _UNSET
+    a.count, a.capacity, a.mask, a.summary, a.sparse = n, scene._capacity, m.data_ptr(), baddr, 0
+    rc = L.igs_las_split_packed(p.addr)
+    if rc:
+        _lib.check(rc, "las_split_batch")
+    rc = L.igs_wait_host_word(baddr + 8, _UNSET, 2_000_000_000, stream)
+    if rc:
+        _lib.check(rc, "las_split_batch")
+    finish_split(scene, int(view[0]), int(view[1]))
+
+
+def split_async(scene, mask, c: SplitConstants, summary=None, sparse=False):
+    """Launch the fused split (igs_las_split_packed / igs_las2d_split): the cooperative
+    pre-pass and the apply pass guarded on the device by the pre-pass totals, with no host
+    round trip in between.  Returns the summary int64[2] = {n_split, flags} (written into
+    ``summary`` when given: device memory or pinned host memory, flags last), not yet read.
+    ``sparse``: the caller knows few parents are masked (3-D: the list-mode apply)."""
+    L = _lib.lib()
+    dev = scene.device
+    n = scene._count
+    m = _mask_tensor(mask, n, dev)
     if summary is None:
-        summary = torch.empty(2, dtype=torch.int64, device=scene.device)
-    alpha, log_alpha, log_gamma, beta = c.device_constants()
-    stream = _lib.stream_handle(scene.device)
+        summary = torch.empty(2, dtype=torch.int64, device=dev)
+    stream = _lib.stream_handle(dev)
     if isinstance(scene, Scene3):
-        pos, ls, rot, op, sh = _column_ptrs(scene)
-        fn = L.igs_las_split_sparse if sparse else L.igs_las_split
-        _lib.check(fn(pos, ls, rot, op, sh, scene._sh.shape[1] * 3, scene.count,
-                      scene.capacity, m.data_ptr(), alpha, log_alpha, log_gamma, beta,
-                      ws.data_ptr(), ws.numel(), summary.data_ptr(), stream), "las_split_batch")
-    else:
-        cols = scene._cols
-        _lib.check(L.igs_las2d_split(cols["positions"].data_ptr(), cols["log_scales"].data_ptr(),
-                                     cols["thetas"].data_ptr(), cols["opacity_logits"].data_ptr(),
-                                     cols["colors"].data_ptr(), scene.count, scene.capacity,
-                                     m.data_ptr(), alpha, log_alpha, log_gamma, beta,
-                                     ws.data_ptr(), ws.numel(), summary.data_ptr(),
-                                     stream), "las_split_batch_2d")
+        p = _plan3(scene, c, stream)
+        a = p.args
+        if p.ws_rows < n:  # the plan holds its workspace tensor (kept alive with the plan)
+            p.ws = _lib.workspace(_lib.query_size(L.igs_las_workspace_bytes, n), dev, "las")
+            a.workspace, a.workspace_bytes, p.ws_rows = p.ws.data_ptr(), p.ws.numel(), n
+        a.count, a.capacity, a.mask = n, scene._capacity, m.data_ptr()
+        a.summary, a.sparse = summary.data_ptr(), 1 if sparse else 0
+        _lib.check(L.igs_las_split_packed(p.addr), "las_split_batch")
+        return summary
+    nbytes = _lib.query_size(L.igs_las_workspace_bytes, n)
+    ws = _lib.workspace(nbytes, dev, "las")
+    alpha, log_alpha, log_gamma, beta = c.device_constants()
+    cols = scene._cols
+    _lib.check(L.igs_las2d_split(cols["positions"].data_ptr(), cols["log_scales"].data_ptr(),
+                                 cols["thetas"].data_ptr(), cols["opacity_logits"].data_ptr(),
+                                 cols["colors"].data_ptr(), scene.count, scene.capacity,
+                                 m.data_ptr(), alpha, log_alpha, log_gamma, beta,
+                                 ws.data_ptr(), ws.numel(), summary.data_ptr(),
+                                 stream), "las_split_batch_2d")
     return summary
 
 
@@ -201,16 +273,15 @@ def finish_split(scene, n_split: int, flags: int):
 
 
 def las_split_batch(scene: Scene3, mask, c: SplitConstants = SplitConstants()) -> Scene3:
-    """Split every masked primitive of a GPU scene in place (las_split.py:158-179)."""
+    """Split every masked primitive of a GPU scene in place (las_split.py:158-179).  Returns
+    once the pre-pass summary is known (count updated, errors raised); the guarded apply pass
+    finishes on the scene's stream."""
     if not isinstance(scene, Scene3):
         raise TypeError(f"expected a paper_2603_08661_b200.core.Scene3, got {type(scene).__name__}")
     if scene.count == 0:
         _mask_tensor(mask, 0, scene.device)  # the length check; nothing to split
         return scene.validate()
-    buf, view = pinned_summary(scene.device)
-    split_async(scene, mask, c, summary=buf)
-    sync(scene.device)
-    finish_split(scene, int(view[0]), int(view[1]))
+    _split3(scene, mask, c)
     return scene.validate()
 
 
@@ -230,7 +301,8 @@ def las_split_batch_2d(scene: Scene2, mask, c: SplitConstants = SplitConstants()
         _mask_tensor(mask, 0, scene.device)
         return scene.validate()
     buf, view = pinned_summary(scene.device)
+    view[1] = _UNSET
     split_async(scene, mask, c, summary=buf)
-    sync(scene.device)
+    wait_summary(scene.device, buf)
     finish_split(scene, int(view[0]), int(view[1]))
     return scene.validate()
