@@ -187,10 +187,13 @@ def densify_step(scene, stats: DensifyStats, cfg: DensifyConfig, step: int) -> D
         # select, then the fused split (pre-pass + device-guarded apply); one host read
         # counts | split summary, written by the kernels straight into pinned host memory
         res, view = _las.pinned_summary(stats._device, 4)
+        view[0] = view[3] = -1  # unwritten: the select's eligible count, the split's flags
         mask, _ = _launch_select(stats, cfg, step, take_cap, counts=res[:2])
         _las.split_async(scene, mask.view(torch.bool), c, summary=res[2:],
                          sparse=4 * take_cap <= n)  # at most a quarter masked: list mode
-        _las.sync(stats._device)
+        # the apply pass may still run: the statistics reset below is ordered after it
+        _las.wait_summary(stats._device, res[2:])
+        _las.wait_word(stats._device, res, 0)
         eligible, n_split, flags = int(view[0]), int(view[2]), int(view[3])
         _las.finish_split(scene, n_split, flags)
     else:

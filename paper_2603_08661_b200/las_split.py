@@ -148,6 +148,12 @@ def wait_summary(device, buf):
                                              _lib.stream_handle(device)), "las_split_batch")
 
 
+def wait_word(device, buf, i):
+    """Wait until word i of the pinned int64 buffer `buf` is no longer -1 (a kernel wrote it)."""
+    _lib.check(_lib.lib().igs_wait_host_word(buf.data_ptr() + 8 * i, _UNSET, 2_000_000_000,
+                                             _lib.stream_handle(device)), "densify_step")
+
+
 def sync(device):
     """Wait for the current stream of `device` (one C call on the raw stream handle)."""
     _lib.check(_lib.lib().igs_stream_synchronize(_lib.stream_handle(device)), "synchronize")
