@@ -697,11 +697,14 @@ def bench_las(args, world, dev, peak, peak_src):
                         "timing": "kernel_ms: 10 back-to-back apply launches between CUDA "
                                   "events; split_device_ms: 10 back-to-back igs_las_split "
                                   "(cooperative pre-pass + guarded apply); ms_per_step: the "
-                                  "public las_split_batch call (host work + one stream sync)"},
+                                  "public las_split_batch call, CUDA events around it (host work, "
+                                  "the launches, the spin on the pinned pre-pass summary; the "
+                                  "apply pass ends before the closing event)"},
            "densify_step": {"ms": round(ds_ms, 4), "n": n, "split": ev.split,
                             "eligible": ev.eligible,
-                            "note": "select (radix top-k, take=ceil(0.05 N)) + LAS + one host "
-                                    "sync, public densify_step()"}}
+                            "note": "select (radix top-k, take=ceil(0.05 N)) + LAS + the "
+                                    "statistics reset, public densify_step(); the host reads "
+                                    "the pinned select count and split summary"}}
     if world == 1 and not args.no_cpu:
         rate, kind, sample = cpu_las_rate()
         res["cpu_baseline"] = {"value": round(rate, 1), "unit": "Gaussians/s", "cores": 1,
