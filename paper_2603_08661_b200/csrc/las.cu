@@ -482,41 +482,110 @@ __global__ void __launch_bounds__(NT) las2d_apply_kernel(
 //     {n_split, flags} to the workspace (the apply's guard) and to the caller's summary.
 //   las_apply_kernel / las2d_apply_kernel with that guard: every block returns before writing
 //     when the host is about to raise, so the scene is untouched as in the reference.
+// One warp's view of a 512-parent tile: lane L holds mask bytes [16 L, 16 L + 16) of the tile
+// as a 16-bit set of masked parents (ascending index = lane-major bit order).
+__device__ __forceinline__ unsigned tile_lane_bits(const uint8_t* __restrict__ mask,
+                                                   long long count, long long tile, bool vec) {
+  const long long i0 = tile * TILE + 16 * (long long)lane_id();
+  unsigned bits = 0;
+  if (vec && i0 + 16 <= count) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(mask + i0));
+    const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const unsigned r = __vcmpne4(w[k], 0u);  // 0xff per nonzero byte
+      bits |= (((r >> 7) & 1u) | ((r >> 14) & 2u) | ((r >> 21) & 4u) | ((r >> 28) & 8u)) << (4 * k);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (i0 + k < count && mask[i0 + k]) bits |= 1u << k;
+  }
+  return bits;
+}
+
+// Fused split pre-pass, one cooperative launch; each CTA owns tiles [t0, t1), one warp per tile
+// (no block barrier per tile).  Phase 1: per tile, the masked count (tile_cnt) and the batch
+// flags of its masked parents; the CTA's total and flags to its own slot.  Grid barrier.
+// Phase 2: every CTA reads all CTA totals / flags, scans its own tiles into slot offsets
+// (tile_off), and CTA 0 writes the summary.  Phase 3 (list mode): each warp writes its tiles'
+// masked parents, in index order, at their slots.
 template <bool D3>
 __global__ void __launch_bounds__(NT) las_prepare_coop_kernel(
     const uint8_t* __restrict__ mask, const float* __restrict__ rot,
     const float* __restrict__ opac, long long count, float beta, long long tiles,
     unsigned* tile_cnt, unsigned long long* tile_off, unsigned long long* cta_tot,
     unsigned* cta_flag, unsigned long long* guard, int64_t* summary, unsigned* list) {
-  __shared__ unsigned warp_cnt[NT / 32];
-  __shared__ unsigned red[NT / 32];
+  constexpr int NW = NT / 32;
+  __shared__ unsigned long long wtot[NW];
+  __shared__ unsigned wflag[NW];
   __shared__ unsigned long long s_pre, s_tot;
   __shared__ unsigned s_flags;
   const long long G = gridDim.x, b = blockIdx.x;
   const long long t0 = b * tiles / G, t1 = (b + 1) * tiles / G;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const bool vec = (((uintptr_t)mask) & 15) == 0;
   unsigned long long tot = 0;
   unsigned flags = 0;
-  for (long long t = t0; t < t1; ++t) {
-    unsigned f = 0;
-    const unsigned n = prepare_tile(mask, D3 ? rot : nullptr, opac, count, beta, t, warp_cnt, f);
-    flags |= f;
-    if (threadIdx.x == 0) {
-      tile_cnt[t] = n;
-      tot += n;
+  if (t1 - t0 <= 2) {  // few tiles per CTA (small batches): the whole CTA on each tile
+    __shared__ unsigned warp_cnt[NW];
+    for (long long t = t0; t < t1; ++t) {
+      unsigned f = 0;
+      const unsigned n = prepare_tile(mask, D3 ? rot : nullptr, opac, count, beta, t, warp_cnt, f);
+      flags |= f;
+      if (threadIdx.x == 0) tile_cnt[t] = n;
+      tot += n;  // block-uniform
     }
+    if (warp != 0) tot = 0;  // counted once, by warp 0
   }
-  if (lane_id() == 0) red[threadIdx.x >> 5] = flags;
-  if (threadIdx.x == 0) {
-    s_pre = 0;
-    s_tot = 0;
-    s_flags = 0;
+  for (long long t = t0 + warp; t1 - t0 > 2 && t < t1; t += NW) {
+    const unsigned bits = tile_lane_bits(mask, count, t, vec);
+    unsigned f = 0;
+    if (opac && bits) {  // opac NULL: counts only (the caller has the flags)
+      const long long i0 = t * TILE + 16 * (long long)lane;
+      float4 q[16];
+      float o[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k)  // every load first, then the checks
+        if ((bits >> k) & 1u) {
+          if (D3) q[k] = __ldg(reinterpret_cast<const float4*>(rot) + i0 + k);
+          o[k] = __ldg(opac + i0 + k);
+        }
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if ((bits >> k) & 1u) {
+          if (D3) {
+            const float n = quat_norm(q[k]);
+            if (!isfinite(n) || n == 0.0f) f |= IGS_LAS_BAD_QUAT;
+            else if (fabsf(n - 1.0f) > 1e-4f) f |= IGS_LAS_RENORM;
+          }
+          const float r = raw_opacity(o[k], beta);
+          if (!(r > 0.0f && r < 1.0f)) f |= IGS_LAS_BAD_OPACITY;
+        }
+    }
+    const unsigned cnt = __reduce_add_sync(0xffffffffu, (unsigned)__popc(bits));
+    flags |= __reduce_or_sync(0xffffffffu, f);
+    if (lane == 0) tile_cnt[t] = cnt;
+    tot += cnt;
+  }
+  if (lane == 0) {
+    wtot[warp] = tot;
+    wflag[warp] = flags;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned f = 0;
-    for (int k = 0; k < NT / 32; ++k) f |= red[k];
-    cta_tot[b] = tot;
-    cta_flag[b] = f;
+    unsigned long long ct = 0;
+    unsigned cf = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      ct += wtot[k];
+      cf |= wflag[k];
+    }
+    cta_tot[b] = ct;
+    cta_flag[b] = cf;
+    s_pre = 0;
+    s_tot = 0;
+    s_flags = 0;
   }
   cooperative_groups::this_grid().sync();
   unsigned long long pre = 0, all = 0;
@@ -533,61 +602,62 @@ __global__ void __launch_bounds__(NT) las_prepare_coop_kernel(
     all += __shfl_down_sync(0xffffffffu, all, o);
   }
   fl = __reduce_or_sync(0xffffffffu, fl);
-  if (lane_id() == 0) {
+  if (lane == 0) {
     atomicAdd(&s_pre, pre);
     atomicAdd(&s_tot, all);
     atomicOr(&s_flags, fl);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long off = s_pre;
-    for (long long t = t0; t < t1; ++t) {  // this CTA's own tile counts (a few per CTA)
-      tile_off[t] = off;
-      off += __ldcg(&tile_cnt[t]);
+  if (b == 0 && threadIdx.x == 0) {
+    guard[0] = s_tot;
+    guard[1] = s_flags;
+    // summary[1] last: a host polling it (igs_wait_host_word) then reads a complete summary
+    summary[0] = (int64_t)s_tot;
+    __threadfence_system();
+    summary[1] = (int64_t)s_flags;
+  }
+  // slot offsets of this CTA's tiles: a block scan of their counts, NT tiles per round
+  unsigned long long carry = s_pre;
+  for (long long base = t0; base < t1; base += NT) {
+    const long long t = base + threadIdx.x;
+    const unsigned long long v = t < t1 ? (unsigned long long)__ldcg(&tile_cnt[t]) : 0ull;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    if (b == 0) {
-      guard[0] = s_tot;
-      guard[1] = s_flags;
-      // summary[1] last: a host polling it (igs_wait_host_word) then reads a complete summary
-      summary[0] = (int64_t)s_tot;
-      __threadfence_system();
-      summary[1] = (int64_t)s_flags;
+    if (lane == 31) wtot[warp] = x;
+    __syncthreads();
+    unsigned long long wpre = 0, round = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      if (k < warp) wpre += wtot[k];
+      round += wtot[k];
     }
+    if (t < t1) tile_off[t] = carry + wpre + x - v;
+    carry += round;
+    __syncthreads();
   }
   if (!list) return;
-  // list mode: the masked parents of this CTA's tiles, in index order, at their slots
-  __syncthreads();
-  __shared__ unsigned wpre[SUBS];
-  for (long long t = t0; t < t1; ++t) {
-    const unsigned long long off = __ldcg(&tile_off[t]);
-    const long long base = t * TILE;
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    bool m[PER];
-    unsigned wrank[PER];
+  __syncthreads();  // this CTA's tile_off writes -> its warps' reads below
+  for (long long t = t0 + warp; t < t1; t += NW) {
+    const unsigned bits = tile_lane_bits(mask, count, t, vec);
+    const unsigned c = (unsigned)__popc(bits);
+    unsigned x = c;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const long long i = base + j * NT + threadIdx.x;
-      m[j] = i < count && mask[i];
-      const unsigned bal = __ballot_sync(0xffffffffu, m[j]);
-      wrank[j] = __popc(bal & lanemask_lt());
-      if (lane == 0) wpre[j * (NT / 32) + warp] = __popc(bal);
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const unsigned v = threadIdx.x < (unsigned)SUBS ? wpre[threadIdx.x] : 0u;
-      unsigned x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-        if (threadIdx.x >= (unsigned)o) x += y;
-      }
-      if (threadIdx.x < (unsigned)SUBS) wpre[threadIdx.x] = x - v;
+    unsigned long long at = __ldcg(&tile_off[t]) + (x - c);
+    const unsigned i0 = (unsigned)(t * TILE + 16 * (long long)lane);
+    unsigned rest = bits;
+    while (rest) {
+      const int k = __ffs(rest) - 1;
+      rest &= rest - 1u;
+      list[at++] = i0 + (unsigned)k;
     }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < PER; ++j)
-      if (m[j]) list[off + wpre[j * (NT / 32) + warp] + wrank[j]] = (unsigned)(base + j * NT + threadIdx.x);
-    __syncthreads();
   }
 }
 
