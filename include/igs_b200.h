@@ -146,10 +146,12 @@ int igs_accumulate_grad_norms(double* grad_sum, const void* grads, int dtype, in
  *   igs_shard_keys        -> all-reduce(sum) hist (int32[IGS_SHARD_HIST_LEN]: 65536 bins of a
  *                            monotone 16-bit digit of the score key, then the eligible count)
  *   igs_shard_boundary    resolve take / boundary digit / need, compact this rank's
- *                            boundary-bucket entries into its record
+ *                            boundary-bucket entries into its record, and write the mask of
+ *                            its rows below the boundary bucket
  *                         -> all-gather records (int64[4 + 2 record_cap] per rank)
  *   igs_shard_finalize    threshold (key, gidx) by radix select over every record; the plan
- *                            (int64[16]) and this rank's mask
+ *                            (int64[16]); completes this rank's mask (the boundary rows taken;
+ *                            cleared when nothing is selected or the records overflowed)
  *   igs_las_split_guarded the split of this shard, guarded by plan[0..1]
  *   igs_shard_child_index gidx of this rank's appended children
  * plan words: [0] this rank's split count if the split may go ahead else 0, [1] batch LAS
@@ -167,8 +169,8 @@ int igs_shard_keys(const double* grad_sum, int64_t accum_count, const double* ed
                    void* workspace, size_t workspace_bytes, void* stream);
 int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64_t* gidx,
                        const float* rotations, const float* opacity_logits, float beta,
-                       int64_t n, int64_t record_cap, int64_t* record, void* workspace,
-                       size_t workspace_bytes, void* stream);
+                       int64_t n, int64_t record_cap, int64_t* record, uint8_t* mask,
+                       void* workspace, size_t workspace_bytes, void* stream);
 int igs_shard_finalize(const int64_t* records, int world, int rank, int64_t record_cap,
                        int64_t n_global, const int64_t* gidx, int64_t n, uint8_t* mask,
                        int64_t* plan, void* workspace, size_t workspace_bytes, void* stream);

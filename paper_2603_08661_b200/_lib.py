@@ -51,8 +51,8 @@ SIGNATURES = {
     "igs_accumulate_grad_norms": (_int, [_vp, _vp, _int, _i64, _vp]),
     "igs_shard_workspace_bytes": (_int, [_i64, _szp]),
     "igs_shard_keys": (_int, [_vp, _i64, _vp, _i64, _dbl, _int, _int, _vp, _vp, _sz, _vp]),
-    "igs_shard_boundary": (_int, [_vp, _i64, _vp, _vp, _vp, _flt, _i64, _i64, _vp, _vp, _sz,
-                                  _vp]),
+    "igs_shard_boundary": (_int, [_vp, _i64, _vp, _vp, _vp, _flt, _i64, _i64, _vp, _vp, _vp,
+                                  _sz, _vp]),
     "igs_shard_finalize": (_int, [_vp, _int, _int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _sz,
                                   _vp]),
     "igs_shard_child_index": (_int, [_vp, _i64, _vp, _vp]),

@@ -52,14 +52,15 @@ struct State {
 static_assert(sizeof(State) <= 256, "state fits its 256-byte slot");
 
 struct Layout {
-  size_t state, keys, total;
+  size_t state, keys, bidx, total;
 };
 
 inline Layout layout(long long n) {
   Layout L;
   L.state = 0;
   L.keys = 256;
-  L.total = align_up(L.keys + sizeof(unsigned long long) * (size_t)n, 256);
+  L.bidx = align_up(L.keys + sizeof(unsigned long long) * (size_t)n, 256);  // u32 per row
+  L.total = align_up(L.bidx + sizeof(unsigned) * (size_t)n, 256);
   return L;
 }
 
@@ -245,7 +246,8 @@ __global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* 
                                                      const long long* __restrict__ gidx,
                                                      const float* rot, const float* opac,
                                                      float beta, long long n, const State* st,
-                                                     long long cap, long long* record) {
+                                                     long long cap, long long* record,
+                                                     uint8_t* mask, unsigned* bidx) {
   __shared__ unsigned s_lt, s_flags;
   if (threadIdx.x == 0) {
     s_lt = 0;
@@ -290,6 +292,9 @@ __global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* 
         ++lt;
         fl |= fu;
       }
+      // the mask of the rows below the boundary bucket (the boundary rows the plan takes are
+      // set by boundary_mask_kernel once the threshold is known)
+      if (i0 + u * NTC < hi) mask[i0 + u * NTC] = dv[u] < B;
       const bool bnd = dv[u] == B;
       const unsigned bal = __ballot_sync(0xffffffffu, bnd);
       if (!bal) continue;
@@ -301,6 +306,7 @@ __global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* 
         const unsigned long long slot = base + __popc(bal & lanelt);
         if ((long long)slot < cap) {
           const long long i = i0 + u * NTC;
+          bidx[slot] = (unsigned)i;
           record[R_HDR + 2 * slot] = (long long)kv[u];
           record[R_HDR + 2 * slot + 1] =
               (long long)((unsigned long long)gidx[i] | ((unsigned long long)fu << 56));
@@ -527,6 +533,32 @@ __global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__
   }
 }
 
+// The mask once the plan is known: compact_kernel wrote every row's (digit < B); this sets the
+// boundary rows the plan takes (this rank's boundary entries, their local rows in bidx), or
+// clears the mask when nothing is selected / the records overflowed (the re-run rewrites it).
+__global__ void __launch_bounds__(NT) boundary_mask_kernel(
+    const unsigned long long* __restrict__ keys, const long long* __restrict__ gidx, long long n,
+    const long long* __restrict__ records, int rank, long long cap, const unsigned* bidx,
+    const long long* plan, uint8_t* mask) {
+  if (plan[P_STATUS] != 0) {
+    for (long long i = blockIdx.x * (long long)NT + threadIdx.x; i < n;
+         i += (long long)gridDim.x * NT)
+      mask[i] = 0;
+    return;
+  }
+  const unsigned long long T = (unsigned long long)plan[P_T];
+  const unsigned long long G = (unsigned long long)plan[P_G];
+  const long long stride = R_HDR + 2 * cap;
+  long long nb = records[rank * stride + R_BCNT];
+  nb = nb < cap ? nb : cap;
+  for (long long s = blockIdx.x * (long long)NT + threadIdx.x; s < nb;
+       s += (long long)gridDim.x * NT) {
+    const long long i = bidx[s];
+    const unsigned long long k = keys[i];
+    if (k < T || (k == T && (unsigned long long)gidx[i] <= G)) mask[i] = 1;
+  }
+}
+
 __global__ void __launch_bounds__(NT) mask_kernel(const unsigned long long* __restrict__ keys,
                                                   const long long* __restrict__ gidx, long long n,
                                                   const long long* plan, uint8_t* mask) {
@@ -600,9 +632,10 @@ int igs_shard_keys(const double* grad_sum, int64_t accum_count, const double* ed
 
 int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64_t* gidx,
                        const float* rotations, const float* opacity_logits, float beta,
-                       int64_t n, int64_t record_cap, int64_t* record, void* workspace,
-                       size_t workspace_bytes, void* stream) {
+                       int64_t n, int64_t record_cap, int64_t* record, uint8_t* mask,
+                       void* workspace, size_t workspace_bytes, void* stream) {
   if (!global_hist || !record || take_cap < 0 || n < 0 || record_cap < 1) return IGS_ERR_ARGUMENT;
+  if (n > 0 && !mask) return IGS_ERR_ARGUMENT;
   if (((uintptr_t)global_hist & 15) || ((uintptr_t)rotations & 15)) return IGS_ERR_ARGUMENT;
   if (n > 0 && !gidx) return IGS_ERR_ARGUMENT;  // opacity_logits NULL: no LAS flags
   shard::Layout L = shard::layout(n);
@@ -619,7 +652,7 @@ int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64
   if (cgrid < 1) cgrid = 1;
   shard::compact_kernel<<<(unsigned)cgrid, shard::NTC, 0, st>>>(
       (const unsigned long long*)(w + L.keys), (const long long*)gidx, rotations, opacity_logits,
-      beta, n, S, record_cap, (long long*)record);
+      beta, n, S, record_cap, (long long*)record, mask, (unsigned*)(w + L.bidx));
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }
@@ -644,8 +677,9 @@ int igs_shard_finalize(const int64_t* records, int world, int rank, int64_t reco
   long long grid = (n + shard::NT - 1) / shard::NT;
   const long long cap = 8LL * (sm_count() > 0 ? sm_count() : 148);
   if (grid > cap) grid = cap;
-  shard::mask_kernel<<<(unsigned)grid, shard::NT, 0, st>>>(
+  shard::boundary_mask_kernel<<<(unsigned)grid, shard::NT, 0, st>>>(
       (const unsigned long long*)(w + L.keys), (const long long*)gidx, n,
+      (const long long*)records, rank, record_cap, (const unsigned*)(w + L.bidx),
       (const long long*)plan, mask);
   IGS_LAUNCH_CHECK();
   return IGS_OK;

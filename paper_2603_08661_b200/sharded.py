@@ -150,8 +150,8 @@ class CudaShardOps:
         rot, op = _flag_columns(scene)
         _lib.check(self.L.igs_shard_boundary(
             hist.data_ptr(), int(take_cap), gidx.data_ptr(), rot, op, float(beta), self.n,
-            int(cap), rec.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
-            _lib.stream_handle()), "densify_step_sharded")
+            int(cap), rec.data_ptr(), self.mask.data_ptr(), self.ws.data_ptr(),
+            self.ws.numel(), _lib.stream_handle()), "densify_step_sharded")
         return rec
 
     def finalize(self, records, rank: int, cap: int, n_global: int, gidx):
