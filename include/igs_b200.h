@@ -59,6 +59,10 @@ int igs_stream_synchronize(void* stream);
  * longer `sentinel`.  After timeout_ns the stream is synchronised instead (an asynchronous
  * kernel fault returns its CUDA error); IGS_ERR_CUDA if the word is still unwritten. */
 int igs_wait_host_word(const int64_t* word, int64_t sentinel, int64_t timeout_ns, void* stream);
+/* Stream-ordered copy of n int64 words from device memory into pinned host memory, then
+ * host[n] = 1 (after a system-scope fence): the host spins on host[n] instead of a stream
+ * synchronise (the sharded step reads its plan while the guarded split still runs). */
+int igs_publish_words(const int64_t* src, int64_t* host, int64_t n, void* stream);
 
 /* L2 set-aside for persisting (evict_last) lines: the fused edge kernel keeps the in-flight
  * views' thinned maps evict_last.  Device-wide (cudaLimitPersistingL2CacheSize), clamped to

@@ -32,6 +32,7 @@ SIGNATURES = {
     "igs_abi_version": (_int, []),
     "igs_stream_synchronize": (_int, [_vp]),
     "igs_wait_host_word": (_int, [_vp, _i64, _i64, _vp]),
+    "igs_publish_words": (_int, [_vp, _vp, _i64, _vp]),
     "igs_l2_set_aside": (_int, [_sz, _szp]),
     "igs_edge_workspace_bytes": (_int, [_i64, _i64, _i64, _int, _szp]),
     "igs_edge_importance": (_int, [_vp, _int, _int, _i64, _i64, _i64, _vp, _int, _vp, _vp, _sz,

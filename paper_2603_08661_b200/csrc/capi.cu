@@ -52,6 +52,25 @@ int igs_stream_synchronize(void* stream) {
   return IGS_OK;
 }
 
+// Copy n int64 words of device memory into pinned host memory, then (system-scope fence)
+// set host[n] = 1: a host spinning on host[n] (igs_wait_host_word) reads complete words while
+// the stream runs on (e.g. the sharded plan, before the split it guards has finished).
+__global__ void publish_words_kernel(const int64_t* src, int64_t* host, int64_t n) {
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) host[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *(volatile int64_t*)(host + n) = 1;
+  }
+}
+
+int igs_publish_words(const int64_t* src, int64_t* host, int64_t n, void* stream) {
+  if (!src || !host || n < 0) return IGS_ERR_ARGUMENT;
+  publish_words_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(src, host, n);
+  IGS_LAUNCH_CHECK();
+  return IGS_OK;
+}
+
 // Spin until the host word (pinned memory a kernel writes) differs from `sentinel`; after
 // `timeout_ns` fall back to synchronising `stream` (so an asynchronous kernel fault surfaces
 // as its CUDA error) and fail with IGS_ERR_CUDA if the word is still unwritten.

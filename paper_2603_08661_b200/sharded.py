@@ -186,12 +186,23 @@ def _rerun(ops, hist, take_cap, comm, gidx, n_global, scene, beta, cap):
     return ops.finalize(comm.all_gather(rec), comm.rank, cap, n_global, gidx)
 
 
-def _read(plan, pinned):
-    buf, view = pinned
-    buf.copy_(plan, non_blocking=True)
+def _publish(plan, pinned):
+    """Stream-ordered copy of the plan into pinned memory with a ready word (the host then
+    reads it without waiting for the split it guards)."""
     if plan.is_cuda:
-        _las.sync(plan.device)
-    return [int(v) for v in view]
+        buf, view = pinned
+        view[PLAN_WORDS] = -1
+        _lib.check(_lib.lib().igs_publish_words(plan.data_ptr(), buf.data_ptr(), PLAN_WORDS,
+                                                _lib.stream_handle(plan.device)),
+                   "densify_step_sharded")
+
+
+def _read(plan, pinned):
+    if not plan.is_cuda:
+        return [int(v) for v in plan.tolist()]
+    buf, view = pinned
+    _las.wait_word(plan.device, buf, PLAN_WORDS)
+    return [int(v) for v in view[:PLAN_WORDS]]
 
 
 def default_record_cap(world: int) -> int:
@@ -360,18 +371,15 @@ def select_candidates_sharded(stats: DensifyStats, cfg: DensifyConfig, step: int
     cap = record_cap or default_record_cap(comm.world)
     hist, (mask, plan) = _protocol(ops, stats, cfg, step, take_cap, comm, gidx, global_count,
                                    scene, beta, cap)
-    pinned = _las.pinned_summary(dev, PLAN_WORDS) if dev.type == "cuda" else _host_buf()
+    pinned = _las.pinned_summary(dev, PLAN_WORDS + 1) if dev.type == "cuda" else None
+    _publish(plan, pinned)
     p = _read(plan, pinned)
     while p[P_STATUS] == STATUS_OVERFLOW:
         mask, plan = _resolve_overflow(ops, hist, take_cap, comm, gidx, global_count, scene, beta,
                                        p[P_MAXB])
+        _publish(plan, pinned)
         p = _read(plan, pinned)
     return (mask.view(torch.bool), p) if return_plan else mask.view(torch.bool)
-
-
-def _host_buf():
-    t = torch.zeros(PLAN_WORDS, dtype=torch.int64)
-    return t, t.numpy()
 
 
 def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: int,
@@ -393,16 +401,17 @@ def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: i
     alpha, log_alpha, log_gamma, beta = c.device_constants()
     gidx = scene._gidx
     cap = default_record_cap(comm.world)
-    pinned = _las.pinned_summary(scene.device, PLAN_WORDS)
+    pinned = _las.pinned_summary(scene.device, PLAN_WORDS + 1)
     hist, (mask, plan) = _protocol(ops, stats, cfg, step, take_cap, comm, gidx, glob.count,
                                    scene, beta, cap)
     while True:
+        _publish(plan, pinned)
         if take_cap > 0:
             _split_guarded(scene, mask, plan, alpha, log_alpha, log_gamma, beta)
             _lib.check(_lib.lib().igs_shard_child_index(gidx.data_ptr(), n, plan.data_ptr(),
                                                         _lib.stream_handle()),
                        "densify_step_sharded")
-        p = _read(plan, pinned)                                    # the event's one host read
+        p = _read(plan, pinned)  # the event's one host read (the split may still be running)
         if p[P_STATUS] != STATUS_OVERFLOW:
             break
         mask, plan = _resolve_overflow(ops, hist, take_cap, comm, gidx, glob.count, scene,
