@@ -162,16 +162,20 @@ __global__ void __launch_bounds__(NT) keys_kernel(KeyParams P) {
 enum Rec { R_LT = 0, R_BCNT = 1, R_LTFLAGS = 2, R_HDR = 4 };
 
 // One block: take, B and need from the merged histogram; clears this rank's record header.
-// Thread t owns the 64 consecutive bins [64 t, 64 t + 64) (16-byte loads); a block scan of
-// the per-thread sums names the owner of rank take-1, which walks its bins.
+// Warp w owns the 2048 consecutive bins [2048 w, 2048 w + 2048), read with coalesced 16-byte
+// loads (lane l: bins 4 (l + 32 k) .. + 3 of the range, k < 16).  A scan of the warp totals
+// names the warp holding rank take-1; it walks its 16 chunks of 128 bins, then the lanes of
+// the chunk, then the lane's 4 bins.
 __global__ void __launch_bounds__(NT) resolve_kernel(const int* __restrict__ hist,
                                                      long long take_cap, State* st,
                                                      long long* record) {
-  __shared__ unsigned warp_sums[32];
+  static_assert(NT == 1024 && NBINS == 32 * 2048, "32 warps x 2048 bins");
+  __shared__ unsigned warp_tot[32];
   __shared__ unsigned long long s_need;
   __shared__ int s_B;
   const unsigned long long ne = (unsigned long long)(unsigned)hist[NBINS];
   const unsigned long long take = ne < (unsigned long long)take_cap ? ne : (unsigned long long)take_cap;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     record[R_LT] = 0;
     record[R_BCNT] = 0;
@@ -180,33 +184,65 @@ __global__ void __launch_bounds__(NT) resolve_kernel(const int* __restrict__ his
     s_B = NBINS;
     s_need = 0;
   }
-  const int4* h4 = reinterpret_cast<const int4*>(hist) + threadIdx.x * 16;
-  int4 hv[16];
-  unsigned sum = 0;
+  const int4* h4 = reinterpret_cast<const int4*>(hist) + warp * 512;
+  unsigned cs[16];  // this lane's 4-bin sum of chunk k
+  unsigned mine = 0;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) hv[k] = __ldcg(h4 + k);
+  for (int half = 0; half < 2; ++half) {  // 8 loads in flight at a time (64 registers)
+    int4 hv[8];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) sum += (unsigned)hv[k].x + (unsigned)hv[k].y + (unsigned)hv[k].z + (unsigned)hv[k].w;
-  unsigned total;
-  const unsigned before = block_exclusive_scan(sum, warp_sums, &total);
+    for (int k = 0; k < 8; ++k) hv[k] = __ldcg(h4 + lane + 32 * (8 * half + k));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      cs[8 * half + k] = (unsigned)hv[k].x + (unsigned)hv[k].y + (unsigned)hv[k].z + (unsigned)hv[k].w;
+      mine += cs[8 * half + k];
+    }
+  }
+  const unsigned wt = __reduce_add_sync(0xffffffffu, mine);
+  if (lane == 0) warp_tot[warp] = wt;
+  __syncthreads();
   if (take > 0) {
     const unsigned long long r = take - 1;
-    if (r >= before && r < (unsigned long long)before + sum) {
+    unsigned long long before = 0;
+    for (int w = 0; w < warp; ++w) before += warp_tot[w];
+    if (r >= before && r < before + wt) {  // warp-uniform: this warp holds rank r
       unsigned long long cum = before;
-      int found = -1;
-      unsigned long long at = 0;
+      bool done = false;
 #pragma unroll
-      for (int k = 0; k < 64; ++k) {  // the owner's bins are in its registers
-        const int4 v = hv[k >> 2];
-        const unsigned c = (unsigned)((k & 3) == 0 ? v.x : (k & 3) == 1 ? v.y : (k & 3) == 2 ? v.z : v.w);
-        if (found < 0 && r < cum + c) {
-          found = k;
-          at = cum;
+      for (int k = 0; k < 16; ++k) {
+        const unsigned ck = __reduce_add_sync(0xffffffffu, cs[k]);
+        if (!done && r < cum + ck) {  // chunk k (warp-uniform): lanes in order, 4 bins each
+          done = true;
+          unsigned x = cs[k];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          const unsigned long long lo = cum + (x - cs[k]);
+          if (r >= lo && r < lo + cs[k]) {
+            const int4 hk = __ldcg(h4 + lane + 32 * k);  // the lane's 4 bins again
+            const unsigned b0 = (unsigned)hk.x, b1 = (unsigned)hk.y, b2 = (unsigned)hk.z;
+            unsigned long long at = lo;
+            int j = 0;
+            if (r >= at + b0) {
+              at += b0;
+              j = 1;
+              if (r >= at + b1) {
+                at += b1;
+                j = 2;
+                if (r >= at + b2) {
+                  at += b2;
+                  j = 3;
+                }
+              }
+            }
+            s_B = warp * 2048 + 4 * (lane + 32 * k) + j;
+            s_need = take - at;
+          }
         }
-        cum += c;
+        cum += ck;
       }
-      s_B = threadIdx.x * 64 + found;
-      s_need = take - at;
     }
   }
   __syncthreads();
