@@ -144,6 +144,18 @@ static __device__ __noinline__ double hypot_glibc_slow(double x, double y) {
   return hypot_kernel(ax, ay);
 }
 
+// The LAS logit-domain check of one parent (las_split.py: logit(sigmoid(o) * beta) needs the
+// float32 value strictly inside (0, 1)), as the pre-pass computes it: e = expf(-o),
+// r = (1 / (1 + e)) * beta.  Fast path without expf: for |o| <= 80, e is finite and positive, so
+// 1 / (1 + e) lies in [1.8e-35, 1]; with 1e-6 <= beta < 1 the rounded product is then > 0 and
+// <= beta < 1.  Anything else (NaN, large |o|, other beta) is evaluated exactly.
+__device__ __forceinline__ bool las_opacity_bad(float o, float beta) {
+  if (fabsf(o) <= 80.0f && beta >= 1e-6f && beta < 1.0f) return false;
+  const float e = expf(-o);
+  const float r = (1.0f / (1.0f + e)) * beta;
+  return !(r > 0.0f && r < 1.0f);
+}
+
 // np.clip(x, 0, 1) on the bit pattern (integer pipe): NaN kept, x <= 0 (incl. -0) -> +0.
 __device__ __forceinline__ double np_clip01_int(double x) {
   long long b = __double_as_longlong(x);

@@ -108,8 +108,7 @@ __device__ __forceinline__ unsigned prepare_tile(const uint8_t* __restrict__ mas
       if (!isfinite(n) || n == 0.0f) flags |= IGS_LAS_BAD_QUAT;
       else if (fabsf(n - 1.0f) > 1e-4f) flags |= IGS_LAS_RENORM;
     }
-    float r = raw_opacity(o[j], beta);
-    if (!(r > 0.0f && r < 1.0f)) flags |= IGS_LAS_BAD_OPACITY;
+    if (las_opacity_bad(o[j], beta)) flags |= IGS_LAS_BAD_OPACITY;
   }
   unsigned w = __reduce_add_sync(0xffffffffu, local);
   flags_out = __reduce_or_sync(0xffffffffu, flags);
@@ -559,8 +558,7 @@ __global__ void __launch_bounds__(NT) las_prepare_coop_kernel(
             if (!isfinite(n) || n == 0.0f) f |= IGS_LAS_BAD_QUAT;
             else if (fabsf(n - 1.0f) > 1e-4f) f |= IGS_LAS_RENORM;
           }
-          const float r = raw_opacity(o[k], beta);
-          if (!(r > 0.0f && r < 1.0f)) f |= IGS_LAS_BAD_OPACITY;
+          if (las_opacity_bad(o[k], beta)) f |= IGS_LAS_BAD_OPACITY;
         }
     }
     const unsigned cnt = __reduce_add_sync(0xffffffffu, (unsigned)__popc(bits));

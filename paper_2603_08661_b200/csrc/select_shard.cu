@@ -52,14 +52,15 @@ struct State {
 static_assert(sizeof(State) <= 256, "state fits its 256-byte slot");
 
 struct Layout {
-  size_t state, keys, bidx, total;
+  size_t state, keys, klo, bidx, total;
 };
 
 inline Layout layout(long long n) {
   Layout L;
   L.state = 0;
-  L.keys = 256;
-  L.bidx = align_up(L.keys + sizeof(unsigned long long) * (size_t)n, 256);  // u32 per row
+  L.keys = 256;  // keys as two u32 arrays: high words [keys, +4n), low words from klo
+  L.klo = align_up(L.keys + sizeof(unsigned) * (size_t)n, 256);
+  L.bidx = align_up(L.klo + sizeof(unsigned) * (size_t)n, 256);  // u32 per row
   L.total = align_up(L.bidx + sizeof(unsigned) * (size_t)n, 256);
   return L;
 }
@@ -96,6 +97,26 @@ __device__ __forceinline__ int key_digit(unsigned long long key) {
   return 1 + (int)(T_HI - t);
 }
 
+// Keys live as two u32 arrays (high, low words): the passes over every row read only the high
+// words; the digit needs the low word only for the NaN key and the |score| < 2^-1010 corner.
+__device__ __forceinline__ unsigned long long key_at(const unsigned* __restrict__ khi,
+                                                     const unsigned* __restrict__ klo, long long i) {
+  return ((unsigned long long)khi[i] << 32) | klo[i];
+}
+// key_digit from the high word; NBINS for an ineligible row (high word 0xffffffff, which no
+// eligible key has); -1 when the low word is needed.
+__device__ __forceinline__ int digit_hi(unsigned h) {
+  if (h == 0xFFFFFFFFu) return NBINS;
+  if (h == 0xFFF80000u) return -1;                 // the NaN key, or a key sharing its high word
+  const unsigned uh = ~h;
+  if (!(uh >> 31)) return DIGIT_NONPOS;            // a negative score
+  const unsigned bh = uh & 0x7FFFFFFFu;
+  if (bh == 0) return -1;                          // |score| < 2^-1022 or zero: b == 0 needs lo
+  unsigned long long t = (unsigned long long)bh >> 10;  // b >> 42
+  t = t < T_LO ? T_LO : (t > T_HI ? T_HI : t);
+  return 1 + (int)(T_HI - t);
+}
+
 __device__ __forceinline__ void block_range(long long n, long long& lo, long long& hi) {
   const long long per = (n + gridDim.x - 1) / gridDim.x;
   lo = min((long long)blockIdx.x * per, n);
@@ -109,7 +130,8 @@ struct KeyParams {
   long long n;
   double thr;
   int warmup, policy;
-  unsigned long long* keys;
+  unsigned* khi;
+  unsigned* klo;
   int* hist;  // NBINS + 1 (last: eligible count)
 };
 
@@ -140,7 +162,8 @@ __global__ void __launch_bounds__(NT) keys_kernel(KeyParams P) {
       else if (P.policy == IGS_POLICY_GRAD) sc = g;
       else sc = ed[u] * g;
       const unsigned long long k = e ? score_key(sc) : kIneligible;
-      P.keys[i] = k;
+      P.khi[i] = (unsigned)(k >> 32);
+      P.klo[i] = (unsigned)k;
       if (e) {
         ++elig;
         const unsigned d = (unsigned)key_digit(k);
@@ -268,17 +291,15 @@ __device__ __forceinline__ unsigned las_flags_of(bool d3, float4 q, float o, flo
     if (!isfinite(nrm) || nrm == 0.0f) f |= IGS_LAS_BAD_QUAT;
     else if (fabsf(nrm - 1.0f) > 1e-4f) f |= IGS_LAS_RENORM;
   }
-  const float e = expf(-o);
-  const float sg = 1.0f / (1.0f + e);
-  const float r = sg * beta;
-  if (!(r > 0.0f && r < 1.0f)) f |= IGS_LAS_BAD_OPACITY;
+  if (las_opacity_bad(o, beta)) f |= IGS_LAS_BAD_OPACITY;
   return f;
 }
 
 constexpr int NTC = 256;  // compact_kernel block
-constexpr int UC = 8;     // compact_kernel keys per thread per step
+constexpr int UC = 4;     // compact_kernel 16-byte high-word loads per thread per trip
 
-__global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* __restrict__ keys,
+__global__ void __launch_bounds__(NTC) compact_kernel(const unsigned* __restrict__ khi,
+                                                     const unsigned* __restrict__ klo,
                                                      const long long* __restrict__ gidx,
                                                      const float* rot, const float* opac,
                                                      float beta, long long n, const State* st,
@@ -292,60 +313,96 @@ __global__ void __launch_bounds__(NTC) compact_kernel(const unsigned long long* 
   __syncthreads();
   if (st->status) return;
   const int B = (int)st->B;
-  long long lo, hi;
-  block_range(n, lo, hi);
+  // this block's rows, in whole trips of CROWS (16-byte aligned high-word loads)
+  constexpr long long CROWS = (long long)NTC * 4 * UC;
+  const long long per = ((n + gridDim.x - 1) / gridDim.x + CROWS - 1) / CROWS * CROWS;
+  const long long lo = min((long long)blockIdx.x * per, n), hi = min(lo + per, n);
   unsigned lt = 0, fl = 0;
-  // the loop runs the same trip count in every lane, so the warp-aggregated appends below see
-  // every lane (inactive lanes carry kIneligible)
-  const long long span = hi - lo;
-  const long long trips = (span + (long long)UC * NTC - 1) / ((long long)UC * NTC);
   const unsigned lanelt = lanemask_lt();
-  for (long long it = 0; it < trips; ++it) {
-    const long long i0 = lo + it * UC * NTC + threadIdx.x;
-    unsigned long long kv[UC];
-    int dv[UC];
-#pragma unroll
-    for (int u = 0; u < UC; ++u) kv[u] = i0 + u * NTC < hi ? keys[i0 + u * NTC] : kIneligible;
-#pragma unroll
-    for (int u = 0; u < UC; ++u) dv[u] = kv[u] == kIneligible ? NBINS : key_digit(kv[u]);
-    // the selected and boundary rows' LAS inputs: every load in flight before the arithmetic
-    float4 qv[UC];
-    float ov[UC];
+  // every lane runs the same trips, so the warp-aggregated appends see every lane
+  for (long long t0 = lo; t0 < hi; t0 += CROWS) {
+    // rows t0 + 4 (threadIdx.x + NTC u) + j: one 16-byte load of high words per u
+    int dv[UC][4];
 #pragma unroll
     for (int u = 0; u < UC; ++u) {
-      qv[u] = make_float4(1.f, 0.f, 0.f, 0.f);
-      ov[u] = 0.f;
-      if (opac && dv[u] <= B) {
-        const long long i = i0 + u * NTC;
-        if (rot) qv[u] = reinterpret_cast<const float4*>(rot)[i];
-        ov[u] = opac[i];
+      const long long r0 = t0 + 4 * ((long long)threadIdx.x + (long long)NTC * u);
+      uint4 hv = make_uint4(~0u, ~0u, ~0u, ~0u);
+      if (r0 + 4 <= hi) {
+        hv = __ldcs(reinterpret_cast<const uint4*>(khi + r0));
+      } else {
+        if (r0 < hi) hv.x = khi[r0];
+        if (r0 + 1 < hi) hv.y = khi[r0 + 1];
+        if (r0 + 2 < hi) hv.z = khi[r0 + 2];
       }
+      dv[u][0] = digit_hi(hv.x);
+      dv[u][1] = digit_hi(hv.y);
+      dv[u][2] = digit_hi(hv.z);
+      dv[u][3] = digit_hi(hv.w);
     }
 #pragma unroll
+    for (int u = 0; u < UC; ++u)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (dv[u][j] < 0) {  // rare: the digit needs the low word
+          const long long i = t0 + 4 * ((long long)threadIdx.x + (long long)NTC * u) + j;
+          dv[u][j] = key_digit(key_at(khi, klo, i));
+        }
+    // the mask of the rows below the boundary bucket (the boundary rows the plan takes are set
+    // by boundary_mask_kernel once the threshold is known): 4 rows per 4-byte store
+#pragma unroll
     for (int u = 0; u < UC; ++u) {
-      const unsigned fu = (opac && dv[u] <= B) ? las_flags_of(rot != nullptr, qv[u], ov[u], beta) : 0u;
-      if (dv[u] < B) {
-        ++lt;
-        fl |= fu;
+      const long long r0 = t0 + 4 * ((long long)threadIdx.x + (long long)NTC * u);
+      const unsigned m = (dv[u][0] < B ? 1u : 0u) | (dv[u][1] < B ? 1u << 8 : 0u) |
+                         (dv[u][2] < B ? 1u << 16 : 0u) | (dv[u][3] < B ? 1u << 24 : 0u);
+      if (r0 + 4 <= hi) {
+        *reinterpret_cast<unsigned*>(mask + r0) = m;
+      } else {
+        for (int j = 0; j < 4; ++j)
+          if (r0 + j < hi) mask[r0 + j] = (uint8_t)((m >> (8 * j)) & 1u);
       }
-      // the mask of the rows below the boundary bucket (the boundary rows the plan takes are
-      // set by boundary_mask_kernel once the threshold is known)
-      if (i0 + u * NTC < hi) mask[i0 + u * NTC] = dv[u] < B;
-      const bool bnd = dv[u] == B;
-      const unsigned bal = __ballot_sync(0xffffffffu, bnd);
-      if (!bal) continue;
-      unsigned long long base = 0;
-      if ((threadIdx.x & 31) == 0)  // one append per warp
-        base = atomicAdd((unsigned long long*)&record[R_BCNT], (unsigned long long)__popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (bnd) {
-        const unsigned long long slot = base + __popc(bal & lanelt);
-        if ((long long)slot < cap) {
-          const long long i = i0 + u * NTC;
-          bidx[slot] = (unsigned)i;
-          record[R_HDR + 2 * slot] = (long long)kv[u];
-          record[R_HDR + 2 * slot + 1] =
-              (long long)((unsigned long long)gidx[i] | ((unsigned long long)fu << 56));
+    }
+    // the selected and boundary rows' LAS flags (every load of a half-trip in flight first),
+    // the count below the boundary bucket and the boundary-bucket records
+#pragma unroll
+    for (int h2 = 0; h2 < UC / 2; ++h2) {
+      float4 qv[8];
+      float ov[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int u = 2 * h2 + (e >> 2), j = e & 3;
+        const long long i = t0 + 4 * ((long long)threadIdx.x + (long long)NTC * u) + j;
+        qv[e] = make_float4(1.f, 0.f, 0.f, 0.f);
+        ov[e] = 0.f;
+        if (opac && dv[u][j] <= B) {
+          if (rot) qv[e] = __ldg(reinterpret_cast<const float4*>(rot) + i);
+          ov[e] = __ldg(opac + i);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int u = 2 * h2 + (e >> 2), j = e & 3;
+        const int d = dv[u][j];
+        const unsigned fu = (opac && d <= B) ? las_flags_of(rot != nullptr, qv[e], ov[e], beta) : 0u;
+        if (d < B) {
+          ++lt;
+          fl |= fu;
+        }
+        const bool bnd = d == B;
+        const unsigned bal = __ballot_sync(0xffffffffu, bnd);
+        if (!bal) continue;
+        unsigned long long base = 0;
+        if ((threadIdx.x & 31) == 0)  // one append per warp
+          base = atomicAdd((unsigned long long*)&record[R_BCNT], (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (bnd) {
+          const unsigned long long slot = base + __popc(bal & lanelt);
+          if ((long long)slot < cap) {
+            const long long i = t0 + 4 * ((long long)threadIdx.x + (long long)NTC * u) + j;
+            bidx[slot] = (unsigned)i;
+            record[R_HDR + 2 * slot] = (long long)key_at(khi, klo, i);
+            record[R_HDR + 2 * slot + 1] =
+                (long long)((unsigned long long)gidx[i] | ((unsigned long long)fu << 56));
+          }
         }
       }
     }
@@ -573,7 +630,8 @@ __global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__
 // boundary rows the plan takes (this rank's boundary entries, their local rows in bidx), or
 // clears the mask when nothing is selected / the records overflowed (the re-run rewrites it).
 __global__ void __launch_bounds__(NT) boundary_mask_kernel(
-    const unsigned long long* __restrict__ keys, const long long* __restrict__ gidx, long long n,
+    const unsigned* __restrict__ khi, const unsigned* __restrict__ klo,
+    const long long* __restrict__ gidx, long long n,
     const long long* __restrict__ records, int rank, long long cap, const unsigned* bidx,
     const long long* plan, uint8_t* mask) {
   if (plan[P_STATUS] != 0) {
@@ -590,12 +648,13 @@ __global__ void __launch_bounds__(NT) boundary_mask_kernel(
   for (long long s = blockIdx.x * (long long)NT + threadIdx.x; s < nb;
        s += (long long)gridDim.x * NT) {
     const long long i = bidx[s];
-    const unsigned long long k = keys[i];
+    const unsigned long long k = key_at(khi, klo, i);
     if (k < T || (k == T && (unsigned long long)gidx[i] <= G)) mask[i] = 1;
   }
 }
 
-__global__ void __launch_bounds__(NT) mask_kernel(const unsigned long long* __restrict__ keys,
+__global__ void __launch_bounds__(NT) mask_kernel(const unsigned* __restrict__ khi,
+                                                  const unsigned* __restrict__ klo,
                                                   const long long* __restrict__ gidx, long long n,
                                                   const long long* plan, uint8_t* mask) {
   const bool ok = plan[P_STATUS] == 0;
@@ -604,7 +663,7 @@ __global__ void __launch_bounds__(NT) mask_kernel(const unsigned long long* __re
   const unsigned long long G = (unsigned long long)plan[P_G];
   for (long long i = blockIdx.x * (long long)NT + threadIdx.x; i < n;
        i += (long long)gridDim.x * NT) {
-    const unsigned long long k = keys[i];
+    const unsigned long long k = key_at(khi, klo, i);
     bool in = false;
     if (ok && k != kIneligible) {
       const int d = key_digit(k);
@@ -660,7 +719,8 @@ int igs_shard_keys(const double* grad_sum, int64_t accum_count, const double* ed
   if (n == 0) return IGS_OK;
   if (!shard::set_smem()) return IGS_ERR_CUDA;
   shard::KeyParams P{grad_sum, accum_count, edge_score, n, grad_threshold, warmup, policy,
-                     (unsigned long long*)((char*)workspace + L.keys), hist};
+                     (unsigned*)((char*)workspace + L.keys), (unsigned*)((char*)workspace + L.klo),
+                     hist};
   shard::keys_kernel<<<shard::grid_for(n), shard::NT, shard::SMEM_BYTES, st>>>(P);
   IGS_LAUNCH_CHECK();
   return IGS_OK;
@@ -682,12 +742,14 @@ int igs_shard_boundary(const int32_t* global_hist, int64_t take_cap, const int64
   shard::resolve_kernel<<<1, shard::NT, 0, st>>>(global_hist, take_cap, S, (long long*)record);
   IGS_LAUNCH_CHECK();
   if (n == 0) return IGS_OK;
-  long long cgrid = (n + shard::NTC * shard::UC - 1) / (shard::NTC * shard::UC);
+  if (n > 0 && ((uintptr_t)mask & 3)) return IGS_ERR_ARGUMENT;  // 4-row mask stores
+  long long cgrid = (n + 4LL * shard::NTC * shard::UC - 1) / (4LL * shard::NTC * shard::UC);
   const long long cmax = 8LL * (sm_count() > 0 ? sm_count() : 148);
   if (cgrid > cmax) cgrid = cmax;
   if (cgrid < 1) cgrid = 1;
   shard::compact_kernel<<<(unsigned)cgrid, shard::NTC, 0, st>>>(
-      (const unsigned long long*)(w + L.keys), (const long long*)gidx, rotations, opacity_logits,
+      (const unsigned*)(w + L.keys), (const unsigned*)(w + L.klo), (const long long*)gidx,
+      rotations, opacity_logits,
       beta, n, S, record_cap, (long long*)record, mask, (unsigned*)(w + L.bidx));
   IGS_LAUNCH_CHECK();
   return IGS_OK;
@@ -714,7 +776,7 @@ int igs_shard_finalize(const int64_t* records, int world, int rank, int64_t reco
   const long long cap = 8LL * (sm_count() > 0 ? sm_count() : 148);
   if (grid > cap) grid = cap;
   shard::boundary_mask_kernel<<<(unsigned)grid, shard::NT, 0, st>>>(
-      (const unsigned long long*)(w + L.keys), (const long long*)gidx, n,
+      (const unsigned*)(w + L.keys), (const unsigned*)(w + L.klo), (const long long*)gidx, n,
       (const long long*)records, rank, record_cap, (const unsigned*)(w + L.bidx),
       (const long long*)plan, mask);
   IGS_LAUNCH_CHECK();
@@ -732,7 +794,8 @@ int igs_shard_mask(const int64_t* gidx, int64_t n, const int64_t* plan, uint8_t*
   const long long cap = 8LL * (sm_count() > 0 ? sm_count() : 148);
   if (grid > cap) grid = cap;
   shard::mask_kernel<<<(unsigned)grid, shard::NT, 0, (cudaStream_t)stream>>>(
-      (const unsigned long long*)((char*)workspace + L.keys), (const long long*)gidx, n,
+      (const unsigned*)((char*)workspace + L.keys), (const unsigned*)((char*)workspace + L.klo),
+      (const long long*)gidx, n,
       (const long long*)plan, mask);
   IGS_LAUNCH_CHECK();
   return IGS_OK;

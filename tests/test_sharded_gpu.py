@@ -66,6 +66,30 @@ def test_world1_degenerate_boundary_bucket(n, world_cap):
         np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("policy,step", [("edge", 500), ("product", 2000)])
+def test_world1_special_scores_large(policy, step):
+    """NaN, signed zeros, negatives, subnormals, huge and infinite scores scattered through a
+    large array (the keys' digits come from their high words, with the low word only for the
+    NaN key and the subnormal corner): bit-exact with the oracle at several take sizes."""
+    import paper_2603_08661_b200 as b
+    from paper_2603_08661_b200 import sharded
+    n = 100_003
+    rng = np.random.default_rng(77)
+    edge = rng.random(n)
+    special = np.array([np.nan, -0.0, 0.0, -1.5, 5e-324, 1e-310, -1e-310, 2.2e-308, 1e300,
+                        np.inf, -np.inf, 3e-19, 4.0, 7.9])
+    pick = rng.choice(n, n // 50, replace=False)
+    edge[pick] = special[rng.integers(0, len(special), len(pick))]
+    grad = rng.exponential(3e-4, n)
+    for cap in (0.001, 0.05, 0.5):
+        cfg = b.DensifyConfig(budget=10 * n, growth_cap=cap, policy=policy)
+        st = _stats(b, grad, 1, edge)
+        got = sharded.select_candidates_sharded(st, cfg, step, n, n).cpu().numpy()
+        warm = OS.is_warmup_step(500, 15000, 500, 3, step)
+        want, _ = OS.select_candidates(grad, edge, warm, policy, 2e-4, cap, n)
+        np.testing.assert_array_equal(got, want, err_msg=f"{policy} cap={cap}")
+
+
 def test_world1_order_semantics():
     import paper_2603_08661_b200 as b
     from paper_2603_08661_b200 import sharded
