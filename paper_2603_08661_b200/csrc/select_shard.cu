@@ -452,9 +452,16 @@ __device__ unsigned long long block_select64(const unsigned long long (&v)[E], c
     __shared__ unsigned long long s_any;
     if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
+    unsigned long long any = 0;
+    bool have = false;
 #pragma unroll
     for (int k = 0; k < E; ++k)
-      if (ok[k]) s_any = v[k];  // benign race: every writer stores a valid value
+      if (ok[k] && !have) {
+        any = v[k];
+        have = true;
+      }
+    const unsigned hb = __ballot_sync(0xffffffffu, have);
+    if (hb && lane_id() == __ffs(hb) - 1) s_any = any;  // benign race: every writer's value is valid
     __syncthreads();
     prefix = s_any & pmask;
     __syncthreads();
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__
 #pragma unroll
   for (int k = 0; k < EMAX; ++k) {
     const long long e = threadIdx.x + (long long)NT * k;
-    const long long r = e / cap, s = e - r * cap;
+    const long long r = (long long)((unsigned)e / (unsigned)cap), s = e - r * cap;  // m < 2^31
     ok[k] = e < m && s < records[r * stride + R_BCNT];
     kv[k] = ok[k] ? (unsigned long long)records[r * stride + R_HDR + 2 * s] : 0ull;
     gv[k] = ok[k] ? (unsigned long long)records[r * stride + R_HDR + 2 * s + 1] : 0ull;
@@ -551,8 +558,17 @@ __global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__
     s_max = 0;
   }
   __syncthreads();
-  atomicMin(&s_min, kmin);
-  atomicMax(&s_max, kmax);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {  // one shared atomic per warp
+    const unsigned long long a = __shfl_down_sync(0xffffffffu, kmin, o);
+    const unsigned long long b = __shfl_down_sync(0xffffffffu, kmax, o);
+    kmin = a < kmin ? a : kmin;
+    kmax = b > kmax ? b : kmax;
+  }
+  if (lane_id() == 0) {
+    atomicMin(&s_min, kmin);
+    atomicMax(&s_max, kmax);
+  }
   __syncthreads();
   const unsigned long long diff = s_min ^ s_max;
   const int top = diff ? 63 - __clzll(diff) : 0;
@@ -601,16 +617,23 @@ __global__ void __launch_bounds__(NT) final_kernel(const long long* __restrict__
     for (int r = 0; r < world; ++r) s_flags |= (unsigned)records[r * stride + R_LTFLAGS];
   }
   __syncthreads();
+  unsigned fsel = 0;
 #pragma unroll
   for (int k = 0; k < EMAX; ++k) {
-    if (!ok[k]) continue;
     const unsigned long long g = gv[k] & 0x00FFFFFFFFFFFFFFull;
-    if (kv[k] < T || (kv[k] == T && g <= G)) {
-      const long long e = threadIdx.x + (long long)NT * k;
-      atomicAdd(&s_k[e / cap], 1ull);
-      atomicOr(&s_flags, (unsigned)(gv[k] >> 56));
+    const bool in = ok[k] && (kv[k] < T || (kv[k] == T && g <= G));
+    if (in) fsel |= (unsigned)(gv[k] >> 56);
+    // the warp's entries are consecutive: at most a few ranks, one atomic per (warp, rank)
+    const unsigned e = threadIdx.x + (unsigned)NT * (unsigned)k;
+    const unsigned r = e / (unsigned)cap;
+    const unsigned sel = __ballot_sync(0xffffffffu, in);
+    if (sel) {
+      const unsigned grp = __match_any_sync(0xffffffffu, r);
+      if (lane_id() == __ffs(grp) - 1 && (sel & grp)) atomicAdd(&s_k[r], (unsigned long long)__popc(sel & grp));
     }
   }
+  fsel = __reduce_or_sync(0xffffffffu, fsel);
+  if (lane_id() == 0 && fsel) atomicOr(&s_flags, fsel);
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long base = (unsigned long long)n_global;
