@@ -45,6 +45,22 @@ try:
     igs.las_split_batch(small, np.ones(64, bool))
 except igs.BudgetError:
     pass
+# large enough for the warp-per-tile LAS pre-pass (> 2 tiles per CTA) in both apply modes,
+# and a sharded select whose length is not a multiple of 4 (the compact pass's row tails)
+nb = 700_001
+posb, lsb, qb, ob, shb = random_cloud(nb, 4, seed=9)
+big = igs.Scene3(posb, lsb, qb, ob, shb, capacity=nb + nb // 10)
+mb = np.random.default_rng(10).random(nb) < 0.05
+igs.las_split_batch(big, mb)
+from paper_2603_08661_b200 import las_split as LS
+big2 = igs.Scene3(posb, lsb, qb, ob, shb, capacity=nb + nb // 10)
+s2 = LS.split_async(big2, torch.from_numpy(mb).cuda(), igs.SplitConstants(), sparse=True)
+LS.finish_split(big2, *(int(v) for v in s2.cpu()))
+st4 = igs.DensifyStats(3001)
+st4._grad_sum.copy_(torch.from_numpy(np.random.default_rng(11).exponential(3e-4, 3001)))
+st4._accum_count = 1
+st4.set_edge_score(np.random.default_rng(12).random(3001))
+print(int(sharded.select_candidates_sharded(st4, cfg, 2000, 3001, 3001).sum()))
 import tempfile
 with tempfile.TemporaryDirectory() as d:
     igs.write_scene(scene, os.path.join(d, "s.igsp"))
