@@ -378,10 +378,16 @@ __device__ __noinline__ void blur_edge_rows(const Params& p, const double* gin, 
 }
 
 template <bool FAST, int CH>
-__device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_first, int cnt) {
+__device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_first, int cnt,
+                          bool shift = false) {
   const int c = threadIdx.x & 127, h = threadIdx.x >> 7;
   const int H = (int)p.H, W = (int)p.W;
   const int r0 = h * SH;
+  if (shift && h == 1) {  // the previous sub-step's last 4 blurred rows -> context rows 0..3;
+                          // this thread overwrites their sources (rows 16..19) below
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s.b[j * BWP + c] = s.b[(SR + j) * BWP + c];
+  }
   if (r0 >= cnt) return;
   const int nr = min(SH, cnt - r0);
   const int gc = clamp_i(x0 - 2 + c, 0, W - 1) - x0 + 2;  // s.g column of the leftmost tap
@@ -459,10 +465,16 @@ __device__ __forceinline__ int dir_bin(const Params& p, double gx, double gy) {
 // rows R .. R+2.  Thread (c, h): magnitude column c (x = x0 - 1 + c), rows h*8 .. h*8+7,
 // sliding a 3x3 window down s.b.  Cells outside the image hold 0 (edge_pipeline.py:97).
 template <bool NMS>
-__device__ void band_sobel(const Params& p, Smem& s, int x0, int y_first, int rq_first, int cnt) {
+__device__ void band_sobel(const Params& p, Smem& s, int x0, int y_first, int rq_first, int cnt,
+                           bool shift = false) {
   const int c = threadIdx.x & 127, h = threadIdx.x >> 7;
   const int H = (int)p.H, W = (int)p.W;
   const int r0 = h * SH;
+  if (shift && h == 1) {  // the previous sub-step's last 2 Sobel rows -> context rows 0..1;
+                          // this thread overwrites their sources (rows 16..17) below
+    s.q[c] = s.q[SR * MWP + c];
+    s.q[MWP + c] = s.q[(SR + 1) * MWP + c];
+  }
   if (r0 >= cnt) return;
   const int nr = min(SH, cnt - r0);
   const int x = x0 - 1 + c;
@@ -676,39 +688,42 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
   unsigned long long t_prev = 0;
   if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev));
 #endif
-  // prologue: gray rows [ya-4, ya+4) -> s.g rows 0..7; blurred [ya-2, ya+2) -> s.b rows 0..3;
+  // prologue: gray rows [ya-4, ya+4+n0) -> s.g rows 0..; blurred [ya-2, ya+2) -> s.b rows 0..3;
   // Sobel rows [ya-1, ya+1) -> s.q rows 0..1
   if (threadIdx.x == 0) s.list_n[0] = 0;
+  const int n0 = min(SR, yb - ya);
   band_gray<CH, F64>(p, s, v, x0, ya - 4, 0, 8, pol_in);
+  band_gray<CH, F64>(p, s, v, x0, ya + 4, 8, n0, pol_in);
   __syncthreads();
   band_blur<FAST, CH>(p, s, x0, ya - 2, 0, 4);
   __syncthreads();
   if (p.nms) band_sobel<true>(p, s, x0, ya - 1, 0, 2);
   else band_sobel<false>(p, s, x0, ya - 1, 0, 2);
   int parity = 0;
-  PHASE_MARK(6);  // prologue (gray 8 rows, blur 4, Sobel 2)
+  PHASE_MARK(6);  // prologue (gray 8 + n0 rows, blur 4, Sobel 2)
+  // Sub-step: four barriers.  The gray rows of sub-step k+1 are converted in sub-step k's finish
+  // phase (s.g rows 8.. are free once the Sobel phase has shifted the context rows), and the
+  // blurred / Sobel context rows are shifted by the threads that overwrite their sources.
   for (int Y = ya; Y < yb; Y += SR) {
     const int n = min(SR, yb - Y);
     const bool more = Y + SR < yb;
+    const bool first = Y == ya;
     if (threadIdx.x < 32) {  // warp 0: L2 prefetch of the next sub-step's input rows, or
                              // (last sub-step) the claim of the next task
       if (more) prefetch_rows<CH, F64>(p, v, x0, xw, Y + SR + 4, min(Y + 2 * SR, yb) + 4, pol_in);
       else claim_next<CH, F64>(p, s, pol_in);
     }
     if (threadIdx.x == 32) s.list_n[parity ^ 1] = 0;  // the next sub-step's list
-    // s.g rows 0..7 hold gray [Y-4, Y+4); new gray rows [Y+4, Y+4+n) -> rows 8 ..
-    band_gray<CH, F64>(p, s, v, x0, Y + 4, 8, n, pol_in);
+    // s.b rows 0..3 hold blurred [Y-2, Y+2) (shifted here); new rows [Y+2, Y+2+n) -> rows 4 ..
+    // (the prologue's Sobel rows 0..1 read only s.b rows 0..3)
+    band_blur<FAST, CH>(p, s, x0, Y + 2, 4, n, !first);
     __syncthreads();
-    if (more) PHASE_MARK(0);
-    else PHASE_MARK(5);  // the last sub-step's gray phase carries the next-task claim
-    // s.b rows 0..3 hold blurred [Y-2, Y+2); new rows [Y+2, Y+2+n) -> rows 4 ..
-    band_blur<FAST, CH>(p, s, x0, Y + 2, 4, n);
-    __syncthreads();
-    PHASE_MARK(1);
-    // s.q rows 0..1 hold Sobel [Y-1, Y+1); new rows [Y+1, Y+1+n) -> rows 2 ..; meanwhile keep
-    // gray rows [Y+n-4, Y+n+4) for the next sub-step
-    if (p.nms) band_sobel<true>(p, s, x0, Y + 1, 2, n);
-    else band_sobel<false>(p, s, x0, Y + 1, 2, n);
+    if (more) PHASE_MARK(1);
+    else PHASE_MARK(5);  // the last sub-step's blur phase carries the next-task claim
+    // s.q rows 0..1 hold Sobel [Y-1, Y+1) (shifted here); new rows [Y+1, Y+1+n) -> rows 2 ..;
+    // meanwhile keep gray rows [Y+n-4, Y+n+4) for the next sub-step
+    if (p.nms) band_sobel<true>(p, s, x0, Y + 1, 2, n, !first);
+    else band_sobel<false>(p, s, x0, Y + 1, 2, n, !first);
     if (more) shift_rows<double, GWP>(s.g, n, 8);
     __syncthreads();
     PHASE_MARK(2);
@@ -721,14 +736,12 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
     }
     __syncthreads();
     PHASE_MARK(3);
+    // the next sub-step's gray rows [Y+SR+4, ...) -> s.g rows 8 .., with this sub-step's finish
+    if (more) band_gray<CH, F64>(p, s, v, x0, Y + SR + 4, 8, min(SR, yb - Y - SR), pol_in);
     band_nms_finish(p, s, v, x0, Y, parity, pol_mid);
     parity ^= 1;
     __syncthreads();
     PHASE_MARK(4);
-    if (more) {  // context rows for the next sub-step (read by the next blur / NMS)
-      shift_rows<double, BWP>(s.b, n, 4);
-      shift_rows<unsigned, MWP>(s.q, n, 2, 4);
-    }
   }
 }
 
