@@ -1546,8 +1546,12 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
     if (const char* e = getenv("IGS_BAND_H"))  // tuning override, clamped to [SR, BAND_H]
       bh = atoi(e) < SR ? SR : (atoi(e) > BAND_H ? BAND_H : atoi(e));
     const int nbands = (int)((p.H + bh - 1) / bh);
-    p.band_h = (int)((p.H + nbands - 1) / nbands);
-    p.TE = p.ncols * nbands;
+    // equal bands, rounded up to whole sub-steps (a partial sub-step costs its barriers and
+    // context work for a few rows): 822 rows -> 6 x 128 + 54 instead of 7 x 118
+    const int eq = (int)((p.H + nbands - 1) / nbands);
+    p.band_h = ((eq + SR - 1) / SR) * SR;
+    if (p.band_h > BAND_H) p.band_h = BAND_H;
+    p.TE = p.ncols * (int)((p.H + p.band_h - 1) / p.band_h);
   } else {
     p.TE = (int)((p.npx + CHUNK - 1) / CHUNK);
   }

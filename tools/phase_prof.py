@@ -22,6 +22,6 @@ for name, kw in (("full", {}), ("no_median", {"median": False})):
     L.igs_debug_edge_phases(buf, 1)
     tot = sum(buf[:7])
     print(name, json.dumps({k: round(100 * buf[i] / tot, 1) for i, k in
-                            enumerate(("gray", "blur", "sobel", "decide", "finish",
-                                       "gray_last+claim", "prologue"))}),
+                            enumerate(("unused", "blur", "sobel", "decide",
+                                       "finish+next gray", "blur_last+claim", "prologue"))}),
           "block-ms", round(tot / 1e6, 1))
