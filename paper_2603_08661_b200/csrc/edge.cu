@@ -53,7 +53,8 @@ constexpr int SH = SR / 2;                   // rows per blur / Sobel strip (two
 #endif
 constexpr int TWM = 124;                     // max output columns per band
 constexpr int BAND_H = 256;                  // max rows per band (tuning override)
-constexpr int BAND_H_DEFAULT = 128;          // rows per band
+constexpr int BAND_H_DEFAULT = 112;          // rows per band (7 sub-steps; measured best of
+                                             // 80-208 for 200 x 822-row views)
 constexpr int GWP = TWM + 8, BWP = 128, MWP = 128;  // row pitches (cells); the blur /
                                                     // Sobel lanes cover 128 columns
 constexpr int GR = SR + 8, BR = SR + 4, QR = SR + 2;        // rows per sub-step + context
@@ -1533,7 +1534,7 @@ int launch(Params& p, void* ws, size_t ws_bytes, cudaStream_t stream) {
   if (p.mode == MODE_FUSED) {
     p.ncols = (int)((p.W + TWM - 1) / TWM);
     p.tw = (int)((p.W + p.ncols - 1) / p.ncols);
-    // band height: 128 rows, unless the batch is too small to give the grid ~1.5 band tasks
+    // band height: 112 rows, unless the batch is too small to give the grid ~1.5 band tasks
     // per CTA, then the tallest of 96 / 64 / 48 / 32 rows that does (measured on one view:
     // 0.134 ms at 128 rows, 0.090 ms at 32; four views: 0.187 -> 0.157 ms at 48)
     int bh = BAND_H_DEFAULT;
