@@ -314,7 +314,7 @@ __device__ __forceinline__ void ld_rgb(const float* a, unsigned long long pol, d
   b = z;
 }
 
-template <int CH, bool F64>
+template <int CH, bool F64, int RPW = 2>  // RPW: rows per warp (cnt <= 8 RPW)
 __device__ void band_gray(const Params& p, Smem& s, int v, int x0, int y_first, int r_first,
                           int cnt, unsigned long long pol) {
   using T = typename std::conditional<F64, double, float>::type;
@@ -336,7 +336,7 @@ __device__ void band_gray(const Params& p, Smem& s, int v, int x0, int y_first, 
   for (int k = 0; k < 4; ++k) xo[k] = clamp_i(x0 - 4 + lane + 32 * k, 0, W - 1) * CH;
   xo[4] = clamp_i(x0 - 4 + 128 + (lane & 3), 0, W - 1) * CH;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < RPW; ++h) {
     const int r = warp + NWARP * h;
     if (r < cnt) {
       const T* row = img + (long long)clamp_i(y_first + r, 0, H - 1) * W * CH;
@@ -346,7 +346,7 @@ __device__ void band_gray(const Params& p, Smem& s, int v, int x0, int y_first, 
     }
   }
   const int r = warp + NWARP * (lane >> 2);
-  if (lane < 8 && r < cnt)
+  if (lane < 4 * RPW && r < cnt)
     s.g[(r_first + r) * GWP + 128 + (lane & 3)] =
         gray(img + (long long)clamp_i(y_first + r, 0, H - 1) * W * CH + xo[4]);
 }
@@ -378,26 +378,26 @@ __device__ __noinline__ void blur_edge_rows(const Params& p, const double* gin, 
   }
 }
 
-template <bool FAST, int CH>
+template <bool FAST, int CH, int RT = SH>  // RT: output rows per thread (the prologue: 2)
 __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_first, int cnt,
                           bool shift = false) {
   const int c = threadIdx.x & 127, h = threadIdx.x >> 7;
   const int H = (int)p.H, W = (int)p.W;
-  const int r0 = h * SH;
+  const int r0 = h * RT;
   if (shift && h == 1) {  // the previous sub-step's last 4 blurred rows -> context rows 0..3;
                           // this thread overwrites their sources (rows 16..19) below
 #pragma unroll
     for (int j = 0; j < 4; ++j) s.b[j * BWP + c] = s.b[(SR + j) * BWP + c];
   }
   if (r0 >= cnt) return;
-  const int nr = min(SH, cnt - r0);
+  const int nr = min(RT, cnt - r0);
   const int gc = clamp_i(x0 - 2 + c, 0, W - 1) - x0 + 2;  // s.g column of the leftmost tap
   const double* gin = s.g + (rb_first + r0) * GWP + gc;
   auto wsym = [&](int di, int dj) { return p.w6[di < 2 ? 2 - di : di - 2][dj < 2 ? 2 - dj : dj - 2]; };
   auto finish = [&](double x) { return (CH == 3) ? (x > 1.0 ? 1.0 : x) : np_clip01_int(x); };
-  double acc[SH];
+  double acc[RT];
 #pragma unroll
-  for (int r = 0; r < SH + 4; ++r) {
+  for (int r = 0; r < RT + 4; ++r) {
     double xv[5];
 #pragma unroll
     for (int dj = 0; dj < 5; ++dj) xv[dj] = gin[r * GWP + dj];
@@ -406,7 +406,7 @@ __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_
 #pragma unroll
     for (int dj = 0; dj < 5; ++dj) {
 #pragma unroll
-      for (int o = 0; o < SH; ++o) {
+      for (int o = 0; o < RT; ++o) {
         const int di = r - o;
         if (di < 0 || di > 4) continue;
         const int t25 = di * 5 + dj;
@@ -422,12 +422,12 @@ __device__ void band_blur(const Params& p, Smem& s, int x0, int y_first, int rb_
   }
   double* bout = s.b + (rb_first + r0) * BWP + c;
   const int y0 = y_first + r0;
-  if (nr == SH) {
+  if (nr == RT) {
 #pragma unroll
-    for (int o = 0; o < SH; ++o) bout[o * BWP] = finish(acc[o]);
+    for (int o = 0; o < RT; ++o) bout[o * BWP] = finish(acc[o]);
   } else {
 #pragma unroll
-    for (int o = 0; o < SH; ++o)
+    for (int o = 0; o < RT; ++o)
       if (o < nr) bout[o * BWP] = finish(acc[o]);
   }
   if (y0 < 0 || y0 + nr > H) blur_edge_rows<FAST, CH>(p, gin, bout, y0, nr);  // rare
@@ -693,10 +693,9 @@ __device__ void run_band(const Params& p, Smem& s, int v, int t, unsigned long l
   // Sobel rows [ya-1, ya+1) -> s.q rows 0..1
   if (threadIdx.x == 0) s.list_n[0] = 0;
   const int n0 = min(SR, yb - ya);
-  band_gray<CH, F64>(p, s, v, x0, ya - 4, 0, 8, pol_in);
-  band_gray<CH, F64>(p, s, v, x0, ya + 4, 8, n0, pol_in);
+  band_gray<CH, F64, 3>(p, s, v, x0, ya - 4, 0, 8 + n0, pol_in);  // every row's loads in flight
   __syncthreads();
-  band_blur<FAST, CH>(p, s, x0, ya - 2, 0, 4);
+  band_blur<FAST, CH, 2>(p, s, x0, ya - 2, 0, 4);  // 2 rows per strip
   __syncthreads();
   if (p.nms) band_sobel<true>(p, s, x0, ya - 1, 0, 2);
   else band_sobel<false>(p, s, x0, ya - 1, 0, 2);
