@@ -540,26 +540,37 @@ __global__ void __launch_bounds__(NT) las_prepare_coop_kernel(
   for (long long t = t0 + warp; t1 - t0 > 2 && t < t1; t += NW) {
     const unsigned bits = tile_lane_bits(mask, count, t, vec);
     unsigned f = 0;
-    if (opac && bits) {  // opac NULL: counts only (the caller has the flags)
-      const long long i0 = t * TILE + 16 * (long long)lane;
-      float4 q[16];
-      float o[16];
+    if (opac && __any_sync(0xffffffffu, bits != 0u)) {  // opac NULL: counts only
+      // the flag inputs in coalesced order: row tile * 512 + 32 k + lane, its mask bit from
+      // the lane holding it (lane 2k + lane / 16, bit lane % 16); two halves of 8 loads each
+      const long long tb = t * TILE;
 #pragma unroll
-      for (int k = 0; k < 16; ++k)  // every load first, then the checks
-        if ((bits >> k) & 1u) {
-          if (D3) q[k] = __ldg(reinterpret_cast<const float4*>(rot) + i0 + k);
-          o[k] = __ldg(opac + i0 + k);
-        }
+      for (int half = 0; half < 2; ++half) {
+        float4 q[8];
+        float o[8];
+        bool m[8];
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if ((bits >> k) & 1u) {
-          if (D3) {
-            const float n = quat_norm(q[k]);
-            if (!isfinite(n) || n == 0.0f) f |= IGS_LAS_BAD_QUAT;
-            else if (fabsf(n - 1.0f) > 1e-4f) f |= IGS_LAS_RENORM;
+        for (int j = 0; j < 8; ++j) {  // every load of the half first, then the checks
+          const int k = 8 * half + j;
+          const unsigned ob = __shfl_sync(0xffffffffu, bits, 2 * k + (lane >> 4));
+          m[j] = (ob >> (lane & 15)) & 1u;
+          const long long i = tb + 32 * k + lane;
+          if (m[j]) {
+            if (D3) q[j] = __ldg(reinterpret_cast<const float4*>(rot) + i);
+            o[j] = __ldg(opac + i);
           }
-          if (las_opacity_bad(o[k], beta)) f |= IGS_LAS_BAD_OPACITY;
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (m[j]) {
+            if (D3) {
+              const float n = quat_norm(q[j]);
+              if (!isfinite(n) || n == 0.0f) f |= IGS_LAS_BAD_QUAT;
+              else if (fabsf(n - 1.0f) > 1e-4f) f |= IGS_LAS_RENORM;
+            }
+            if (las_opacity_bad(o[j], beta)) f |= IGS_LAS_BAD_OPACITY;
+          }
+      }
     }
     const unsigned cnt = __reduce_add_sync(0xffffffffu, (unsigned)__popc(bits));
     flags |= __reduce_or_sync(0xffffffffu, f);
