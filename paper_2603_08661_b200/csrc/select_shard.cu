@@ -296,9 +296,14 @@ __device__ __forceinline__ unsigned las_flags_of(bool d3, float4 q, float o, flo
 }
 
 constexpr int NTC = 256;  // compact_kernel block
-constexpr int UC = 4;     // compact_kernel 16-byte high-word loads per thread per trip
+// compact_kernel: 16-byte high-word loads per thread per trip (even: the flag gathers run in
+// halves of 8 rows) and resident blocks per SM (64 registers): UC 2 at 4 blocks per SM
+// measured 31 us at 6M rows against 37 us for UC 4 at 3 blocks and 45-49 us otherwise
+constexpr int UC = 2;
+constexpr int CMINB = 4;
+static_assert(UC % 2 == 0, "compact trips are processed in halves of 8 rows");
 
-__global__ void __launch_bounds__(NTC) compact_kernel(const unsigned* __restrict__ khi,
+__global__ void __launch_bounds__(NTC, CMINB) compact_kernel(const unsigned* __restrict__ khi,
                                                      const unsigned* __restrict__ klo,
                                                      const long long* __restrict__ gidx,
                                                      const float* rot, const float* opac,
