@@ -51,6 +51,8 @@ enum igs_las_flags {
 
 const char* igs_strerror(int status);
 const char* igs_last_cuda_error(void);
+/* 2 since round 2 (igs_shard_boundary takes the mask; the packed LAS call and the pinned-word
+ * helpers were added). */
 int igs_abi_version(void);
 /* cudaStreamSynchronize(stream): the host half of a synchronous call whose kernels write
  * their result into pinned host memory (e.g. igs_las_split's summary). */

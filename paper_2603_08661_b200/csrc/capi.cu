@@ -43,7 +43,9 @@ const char* igs_strerror(int status) {
 
 const char* igs_last_cuda_error(void) { return igs::g_cuda_error; }
 
-int igs_abi_version(void) { return 1; }
+// 2: igs_shard_boundary takes the mask (round 2); igs_las_split_packed, igs_las_split_sparse,
+//    igs_wait_host_word, igs_publish_words added
+int igs_abi_version(void) { return 2; }
 
 // Wait for `stream` (the host half of a synchronous call such as las_split_batch, whose
 // kernels write their summary into pinned host memory).

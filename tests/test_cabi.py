@@ -47,7 +47,7 @@ def test_ctypes_table_matches_header():
 
 def test_host_only_queries(lib):
     from paper_2603_08661_b200 import _lib
-    assert lib.igs_abi_version() >= 1
+    assert lib.igs_abi_version() >= 2
     assert lib.igs_strerror(0) == b"ok"
     assert lib.igs_strerror(_lib.IGS_ERR_WORKSPACE) == b"workspace too small"
     out = C.c_size_t(0)
