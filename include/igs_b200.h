@@ -139,7 +139,10 @@ int igs_select_candidates(const double* grad_sum, int64_t accum_count, const dou
 
 /* Trainer-side statistics (splat2d.py:393-394 + densify_controller.py:54-63): grad_sum[i] +=
  * hypot(grads[2i], grads[2i+1]) in float64 (glibc hypot, as np.hypot); grads (n, 2) of dtype
- * IGS_F32 / IGS_F64.  The caller increments the accumulation count. */
+ * IGS_F32 / IGS_F64.  The caller increments the accumulation count.  dtype | IGS_ACCUM_STORE:
+ * the first accumulation after a reset, grad_sum[i] = 0.0 + hypot(...) without reading
+ * grad_sum (the reset's zeros are never written). */
+#define IGS_ACCUM_STORE 0x100
 int igs_accumulate_grad_norms(double* grad_sum, const void* grads, int dtype, int64_t n,
                               void* stream);
 

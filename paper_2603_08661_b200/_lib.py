@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("IGS_LIB") or os.path.join(HERE, "libigs_b200.so")  # 
 
 IGS_OK, IGS_ERR_ARGUMENT, IGS_ERR_CUDA, IGS_ERR_WORKSPACE, IGS_ERR_UNSUPPORTED = range(5)
 IGS_F32, IGS_F64 = 0, 1
+IGS_ACCUM_STORE = 0x100  # igs_accumulate_grad_norms: store 0.0 + h (first accumulation)
 IGS_EDGE_NO_NMS, IGS_EDGE_NO_MEDIAN = 1, 2
 IGS_POLICY = {"product": 0, "edge": 1, "grad": 2}
 IGS_LAS_BAD_QUAT, IGS_LAS_BAD_OPACITY, IGS_LAS_RENORM = 1, 2, 4

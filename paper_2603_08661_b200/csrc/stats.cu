@@ -34,7 +34,9 @@ template <>
 struct Pair<float> { using V = float2; };
 
 // PAIR: g is aligned for one (gx, gy) vector load per primitive.
-template <typename T, bool PAIR>
+// STORE: the first accumulation after a reset (grad_sum holds no values yet): grad_sum[i] =
+// 0.0 + h, what numpy's zeros + h gives, without reading the stale buffer.
+template <typename T, bool PAIR, bool STORE>
 __global__ void __launch_bounds__(NT) accumulate_kernel(double* __restrict__ grad_sum,
                                                         const T* __restrict__ g, long long n) {
   const long long base = (long long)blockIdx.x * NT * U + threadIdx.x;
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(NT) accumulate_kernel(double* __restrict__ gra
         gx[u] = g[2 * i];
         gy[u] = g[2 * i + 1];
       }
-      sum[u] = grad_sum[i];
+      sum[u] = STORE ? 0.0 : grad_sum[i];
     }
   }
 #pragma unroll
@@ -75,23 +77,25 @@ extern "C" {
 
 int igs_accumulate_grad_norms(double* grad_sum, const void* grads, int dtype, int64_t n,
                               void* stream) {
+  const bool store = (dtype & IGS_ACCUM_STORE) != 0;
+  dtype &= ~IGS_ACCUM_STORE;
   if (n < 0 || (dtype != IGS_F32 && dtype != IGS_F64)) return IGS_ERR_ARGUMENT;
   if (n == 0) return IGS_OK;
   if (!grad_sum || !grads) return IGS_ERR_ARGUMENT;
   const unsigned blocks = (unsigned)((n + stats::NT * stats::U - 1) / (stats::NT * stats::U));
   cudaStream_t st = (cudaStream_t)stream;
   const uintptr_t a = (uintptr_t)grads;
+  const bool pair = a % (dtype == IGS_F64 ? 16 : 8) == 0;
+#define IGS_ACCUM(T, P, S) \
+  stats::accumulate_kernel<T, P, S><<<blocks, stats::NT, 0, st>>>(grad_sum, (const T*)grads, n)
   if (dtype == IGS_F64) {
-    if (a % 16 == 0)
-      stats::accumulate_kernel<double, true><<<blocks, stats::NT, 0, st>>>(grad_sum, (const double*)grads, n);
-    else
-      stats::accumulate_kernel<double, false><<<blocks, stats::NT, 0, st>>>(grad_sum, (const double*)grads, n);
+    if (store) { if (pair) IGS_ACCUM(double, true, true); else IGS_ACCUM(double, false, true); }
+    else { if (pair) IGS_ACCUM(double, true, false); else IGS_ACCUM(double, false, false); }
   } else {
-    if (a % 8 == 0)
-      stats::accumulate_kernel<float, true><<<blocks, stats::NT, 0, st>>>(grad_sum, (const float*)grads, n);
-    else
-      stats::accumulate_kernel<float, false><<<blocks, stats::NT, 0, st>>>(grad_sum, (const float*)grads, n);
+    if (store) { if (pair) IGS_ACCUM(float, true, true); else IGS_ACCUM(float, false, true); }
+    else { if (pair) IGS_ACCUM(float, true, false); else IGS_ACCUM(float, false, false); }
   }
+#undef IGS_ACCUM
   IGS_LAUNCH_CHECK();
   return IGS_OK;
 }

@@ -39,22 +39,39 @@ class DensifyStats:
 
     def __init__(self, count: int, device=None):
         self._device = torch.device(device) if device is not None else _dev()
-        self._grad_sum = torch.zeros(count, dtype=torch.float64, device=self._device)
+        self._new(count)
+
+    def _new(self, count: int):
+        # rows: gradient-norm sums, edge scores.  A reset does not fill them: a row marked
+        # pending reads as zeros (zeroed on first access), the first position-gradient
+        # accumulation stores instead of adding, and an assignment of the edge scores
+        # overwrites the row -- so in the trainer's loop the reset's zeros are never written.
+        self._buf = torch.empty(2, count, dtype=torch.float64, device=self._device)
+        self._pending = [True, True]
         self._accum_count = 0
-        self._edge = torch.zeros(count, dtype=torch.float64, device=self._device)
+
+    def _row(self, k: int) -> torch.Tensor:
+        if self._pending[k]:
+            self._buf[k].zero_()
+            self._pending[k] = False
+        return self._buf[k]
+
+    @property
+    def _grad_sum(self) -> torch.Tensor:
+        return self._row(0)
 
     def __len__(self):
-        return self._grad_sum.shape[0]
+        return self._buf.shape[1]
 
     @property
     def grad_norm(self):
         if self._accum_count == 0:
-            return torch.zeros_like(self._grad_sum)
+            return torch.zeros(len(self), dtype=torch.float64, device=self._device)
         return self._grad_sum / self._accum_count
 
     @property
     def edge_score(self):
-        return self._edge
+        return self._row(1)
 
     @edge_score.setter
     def edge_score(self, values):
@@ -64,14 +81,12 @@ class DensifyStats:
         if v.ndim != 1 or v.shape[0] != len(self):
             raise ValueError(f"edge score length {tuple(v.shape)} does not match stats length "
                              f"({len(self)},)")
-        self._edge.copy_(v.to(self._device, torch.float64))
+        self._buf[1].copy_(v.to(self._device, torch.float64))
+        self._pending[1] = False
 
     def reset(self, count: int | None = None):
-        if count is None:
-            count = len(self)
-        both = torch.zeros(2, count, dtype=torch.float64, device=self._device)  # one fill
-        self._grad_sum, self._edge = both[0], both[1]
-        self._accum_count = 0
+        """Fresh zero statistics (new buffers, as the reference's new arrays; no fill kernel)."""
+        self._new(len(self) if count is None else count)
 
     def set_edge_score(self, values):
         self.edge_score = values
@@ -85,7 +100,7 @@ def accumulate_grads(stats: DensifyStats, step_grad_norms) -> DensifyStats:
     if tuple(t.shape) != tuple(stats._grad_sum.shape):
         raise ValueError(f"gradient norms length {tuple(t.shape)} does not match stats length "
                          f"{tuple(stats._grad_sum.shape)}")
-    stats._grad_sum += t
+    stats._grad_sum.add_(t)
     stats._accum_count += 1
     return stats
 
@@ -102,9 +117,12 @@ def accumulate_position_grads(stats: DensifyStats, grad_xy) -> DensifyStats:
         raise ValueError(f"positional gradients {tuple(g.shape)} do not match stats length "
                          f"{len(stats)} (need (N, 2))")
     L = _lib.lib()
-    _lib.check(L.igs_accumulate_grad_norms(stats._grad_sum.data_ptr(), g.data_ptr(),
-                                           _lib.IGS_F64 if g.dtype == torch.float64 else _lib.IGS_F32,
+    dtype = _lib.IGS_F64 if g.dtype == torch.float64 else _lib.IGS_F32
+    if stats._pending[0]:                 # first accumulation since the reset: store 0.0 + h
+        dtype |= _lib.IGS_ACCUM_STORE
+    _lib.check(L.igs_accumulate_grad_norms(stats._buf[0].data_ptr(), g.data_ptr(), dtype,
                                            len(stats), _lib.stream_handle()), "accumulate_grads")
+    stats._pending[0] = False
     stats._accum_count += 1
     return stats
 

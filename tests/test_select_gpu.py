@@ -166,3 +166,40 @@ def test_hypot_bit_exact_wide_range():
     np.testing.assert_array_equal(got.view(np.int64)[~np.isnan(want)],
                                   want.view(np.int64)[~np.isnan(want)])
     assert np.isnan(got[np.isnan(want)]).all()
+
+
+def test_stats_reset_is_lazy_and_exact():
+    """DensifyStats.reset writes nothing: pending rows read as zeros, the first position-gradient
+    accumulation stores 0.0 + h (IGS_ACCUM_STORE), an edge-score assignment overwrites, and the
+    selection sees the same values as after an explicit zero fill (densify_controller.py:23-63)."""
+    b = B()
+    rng = np.random.default_rng(5)
+    n = 50_001
+    st = b.DensifyStats(n)
+    g1 = rng.standard_normal((n, 2))
+    b.accumulate_position_grads(st, g1)
+    st._buf.fill_(np.nan)            # stale contents must never leak through a reset
+    st.reset(n + 7)
+    assert len(st) == n + 7
+    assert torch.equal(st.grad_norm, torch.zeros(n + 7, dtype=torch.float64, device="cuda"))
+    st._buf.fill_(np.nan)
+    g2 = (rng.standard_normal((n + 7, 2)) * 3).astype(np.float32)
+    g2[0] = [-0.0, -0.0]
+    b.accumulate_position_grads(st, g2)
+    b.accumulate_position_grads(st, g2.astype(np.float64))
+    with np.errstate(all="ignore"):
+        want = (0.0 + np.hypot(g2[:, 0], g2[:, 1]).astype(np.float64)) + np.hypot(
+            g2[:, 0].astype(np.float64), g2[:, 1].astype(np.float64))
+    got = st._grad_sum.cpu().numpy()
+    np.testing.assert_array_equal(got.view(np.int64), want.view(np.int64))
+    assert torch.equal(st.edge_score, torch.zeros(n + 7, dtype=torch.float64, device="cuda"))
+    st.reset()
+    st._buf.fill_(np.nan)
+    e = rng.uniform(0, 1, n + 7)
+    st.edge_score = e
+    assert torch.equal(st.edge_score.cpu(), torch.from_numpy(e))
+    assert torch.equal(st._grad_sum, torch.zeros(n + 7, dtype=torch.float64, device="cuda"))
+    st.reset()
+    st._buf.fill_(np.nan)
+    b.accumulate_grads(st, np.ones(n + 7))
+    assert torch.equal(st._grad_sum.cpu(), torch.ones(n + 7, dtype=torch.float64))
