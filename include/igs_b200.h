@@ -184,6 +184,36 @@ int igs_shard_finalize(const int64_t* records, int world, int rank, int64_t reco
                        int64_t n_global, const int64_t* gidx, int64_t n, uint8_t* mask,
                        int64_t* plan, void* workspace, size_t workspace_bytes, void* stream);
 int igs_shard_child_index(int64_t* gidx, int64_t count, const int64_t* plan, void* stream);
+/* The rest of an event in one call (igs_shard_finalize, then igs_publish_words of the plan into
+ * the pinned host_plan[0..plan_words) with host_plan[plan_words] = -1 beforehand and 1 last,
+ * then -- when `split` -- igs_las_split_guarded of the shard under the plan and
+ * igs_shard_child_index): the same launches in the same stream order as the four calls, one
+ * host->library transition instead of four. */
+typedef struct IgsShardEventArgs {
+  const int64_t* records;
+  int32_t world, rank;
+  int64_t record_cap, n_global;
+  int64_t* gidx;
+  int64_t n;
+  uint8_t* mask;
+  int64_t* plan;
+  void* shard_workspace;
+  size_t shard_workspace_bytes;
+  int64_t* host_plan;
+  int64_t plan_words;
+  int32_t split, dims;
+  float* positions;
+  float* log_scales;
+  float* rotations;
+  float* opacity_logits;
+  float* sh_or_colors;
+  int64_t sh_floats, reserved_rows;
+  float alpha, log_alpha, log_gamma, beta;
+  void* las_workspace;
+  size_t las_workspace_bytes;
+  void* stream;
+} IgsShardEventArgs;
+int igs_shard_event(const IgsShardEventArgs* args);
 /* This rank's mask for a plan computed outside igs_shard_finalize (the path for boundary
  * buckets of more than 32768 entries over all ranks, e.g. every score equal). */
 int igs_shard_mask(const int64_t* gidx, int64_t n, const int64_t* plan, uint8_t* mask,

@@ -66,6 +66,7 @@ SIGNATURES = {
     "igs_las_split": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt, _flt,
                              _flt, _vp, _sz, _vp, _vp]),
     "igs_las_split_packed": (_int, [_vp]),
+    "igs_shard_event": (_int, [_vp]),
     "igs_las_split_sparse": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _flt, _flt,
                                     _flt, _flt, _vp, _sz, _vp, _vp]),
     "igs_las2d_split": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _flt, _flt, _flt, _flt,
@@ -137,6 +138,19 @@ class LasSplitArgs(C.Structure):
                 ("log_gamma", _flt), ("beta", _flt), ("workspace", _vp),
                 ("workspace_bytes", _sz), ("summary", _vp), ("stream", _vp),
                 ("sparse", C.c_int32), ("reserved", C.c_int32)]
+
+
+class ShardEventArgs(C.Structure):
+    """Mirror of IgsShardEventArgs (include/igs_b200.h)."""
+    _fields_ = [("records", _vp), ("world", C.c_int32), ("rank", C.c_int32),
+                ("record_cap", _i64), ("n_global", _i64), ("gidx", _vp), ("n", _i64),
+                ("mask", _vp), ("plan", _vp), ("shard_workspace", _vp),
+                ("shard_workspace_bytes", _sz), ("host_plan", _vp), ("plan_words", _i64),
+                ("split", C.c_int32), ("dims", C.c_int32), ("positions", _vp),
+                ("log_scales", _vp), ("rotations", _vp), ("opacity_logits", _vp),
+                ("sh_or_colors", _vp), ("sh_floats", _i64), ("reserved_rows", _i64),
+                ("alpha", _flt), ("log_alpha", _flt), ("log_gamma", _flt), ("beta", _flt),
+                ("las_workspace", _vp), ("las_workspace_bytes", _sz), ("stream", _vp)]
 
 
 def stream_handle(device=None) -> int:

@@ -105,4 +105,23 @@ int igs_l2_set_aside(size_t bytes, size_t* granted) {
   return IGS_OK;
 }
 
+
+// The tail of a sharded densify event in one call (include/igs_b200.h IgsShardEventArgs).
+int igs_shard_event(const IgsShardEventArgs* a) {
+  if (!a || !a->host_plan || a->plan_words < 0) return IGS_ERR_ARGUMENT;
+  int rc = igs_shard_finalize(a->records, a->world, a->rank, a->record_cap, a->n_global, a->gidx,
+                              a->n, a->mask, a->plan, a->shard_workspace,
+                              a->shard_workspace_bytes, a->stream);
+  if (rc) return rc;
+  *(volatile int64_t*)(a->host_plan + a->plan_words) = -1;  // the previous read is complete
+  rc = igs_publish_words(a->plan, a->host_plan, a->plan_words, a->stream);
+  if (rc || !a->split) return rc;
+  rc = igs_las_split_guarded(a->positions, a->log_scales, a->rotations, a->opacity_logits,
+                             a->sh_or_colors, a->sh_floats, a->dims, a->n, a->reserved_rows,
+                             a->mask, a->alpha, a->log_alpha, a->log_gamma, a->beta, a->plan,
+                             a->las_workspace, a->las_workspace_bytes, a->stream);
+  if (rc) return rc;
+  return igs_shard_child_index(a->gidx, a->n, a->plan, a->stream);
+}
+
 }  // extern "C"

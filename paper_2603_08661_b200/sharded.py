@@ -47,6 +47,7 @@ library, and there is no CPU fallback.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -164,6 +165,43 @@ class CudaShardOps:
         return mask, self.plan
 
 
+    def event(self, records, comm, cap: int, n_global: int, gidx, scene, consts, pinned,
+              split: bool):
+        """finalize -> publish the plan -> (split, child indices) in one library call
+        (igs_shard_event); the same launches, in the same order, as the separate calls."""
+        a = self.__dict__.get("_ev")
+        if a is None:
+            a = self._ev = _lib.ShardEventArgs()
+            self._ev_addr = ctypes.addressof(a)
+        records = records.contiguous()
+        self._ev_records = records          # alive until the next event on this stream
+        a.records, a.world, a.rank = records.data_ptr(), comm.world, comm.rank
+        a.record_cap, a.n_global, a.gidx, a.n = int(cap), int(n_global), gidx.data_ptr(), self.n
+        a.mask, a.plan = self.mask.data_ptr(), self.plan.data_ptr()
+        a.shard_workspace, a.shard_workspace_bytes = self.ws.data_ptr(), self.ws.numel()
+        a.host_plan, a.plan_words = pinned[0].data_ptr(), PLAN_WORDS
+        a.split = 1 if split else 0
+        if split:
+            if hasattr(scene, "_rot"):
+                cols = (scene._pos, scene._ls, scene._rot, scene._op, scene._sh)
+                a.sh_floats, a.dims = scene._sh.shape[1] * 3, 3
+            else:
+                c2 = scene._cols
+                cols = (c2["positions"], c2["log_scales"], c2["thetas"], c2["opacity_logits"],
+                        c2["colors"])
+                a.sh_floats, a.dims = 3, 2
+            (a.positions, a.log_scales, a.rotations, a.opacity_logits,
+             a.sh_or_colors) = (t.data_ptr() for t in cols)
+            a.reserved_rows = scene.reserved_rows
+            a.alpha, a.log_alpha, a.log_gamma, a.beta = consts
+            ws = _lib.workspace(_lib.query_size(self.L.igs_las_workspace_bytes, self.n),
+                                self.device, "las")
+            a.las_workspace, a.las_workspace_bytes = ws.data_ptr(), ws.numel()
+        a.stream = _lib.stream_handle()
+        _lib.check(self.L.igs_shard_event(self._ev_addr), "densify_step_sharded")
+        return self.mask, self.plan
+
+
 def _flag_columns(scene):
     """(rotations or None, opacity_logits) device pointers for the LAS flags of the selected
     parents; no scene (selection only): no flags."""
@@ -174,11 +212,16 @@ def _flag_columns(scene):
     return None, scene._opacity_logits.data_ptr()
 
 
-def _protocol(ops, stats, cfg, step, take_cap, comm, gidx, n_global, scene, beta, cap):
-    """The two collective rounds of one event; everything stays on the device."""
+def _exchange(ops, stats, cfg, step, take_cap, comm, gidx, scene, beta, cap):
+    """The two collective rounds of one event (histogram, boundary records), on the device."""
     hist = comm.all_reduce_sum_(ops.keys(stats, cfg, step))                  # round 1
     rec = ops.boundary(hist, take_cap, gidx, scene, beta, cap)
-    return hist, ops.finalize(comm.all_gather(rec), comm.rank, cap, n_global, gidx)  # round 2
+    return hist, comm.all_gather(rec)                                        # round 2
+
+
+def _protocol(ops, stats, cfg, step, take_cap, comm, gidx, n_global, scene, beta, cap):
+    hist, records = _exchange(ops, stats, cfg, step, take_cap, comm, gidx, scene, beta, cap)
+    return hist, ops.finalize(records, comm.rank, cap, n_global, gidx)
 
 
 def _rerun(ops, hist, take_cap, comm, gidx, n_global, scene, beta, cap):
@@ -402,20 +445,22 @@ def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: i
     gidx = scene._gidx
     cap = default_record_cap(comm.world)
     pinned = _las.pinned_summary(scene.device, PLAN_WORDS + 1)
-    hist, (mask, plan) = _protocol(ops, stats, cfg, step, take_cap, comm, gidx, glob.count,
-                                   scene, beta, cap)
+    hist, records = _exchange(ops, stats, cfg, step, take_cap, comm, gidx, scene, beta, cap)
+    if isinstance(ops, CudaShardOps):   # finalize, publish, split, child indices: one call
+        mask, plan = ops.event(records, comm, cap, glob.count, gidx, scene,
+                               (alpha, log_alpha, log_gamma, beta), pinned, take_cap > 0)
+    else:
+        mask, plan = ops.finalize(records, comm.rank, cap, glob.count, gidx)
+        _launch_split(scene, mask, plan, pinned, take_cap, gidx, n, alpha, log_alpha, log_gamma,
+                      beta)
     while True:
-        _publish(plan, pinned)
-        if take_cap > 0:
-            _split_guarded(scene, mask, plan, alpha, log_alpha, log_gamma, beta)
-            _lib.check(_lib.lib().igs_shard_child_index(gidx.data_ptr(), n, plan.data_ptr(),
-                                                        _lib.stream_handle()),
-                       "densify_step_sharded")
         p = _read(plan, pinned)  # the event's one host read (the split may still be running)
         if p[P_STATUS] != STATUS_OVERFLOW:
             break
         mask, plan = _resolve_overflow(ops, hist, take_cap, comm, gidx, glob.count, scene,
                                        beta, p[P_MAXB])            # nothing was written
+        _launch_split(scene, mask, plan, pinned, take_cap, gidx, n, alpha, log_alpha, log_gamma,
+                      beta)
     split = p[P_TAKE] if p[P_STATUS] == STATUS_OK else 0
     if split and p[P_FLAGS] & _lib.IGS_LAS_BAD_OPACITY:
         raise ValueError("logit requires all values strictly inside (0, 1)")
@@ -428,6 +473,17 @@ def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: i
     glob.count += split
     stats.reset(scene.count)
     return DensifyEvent(step=step, eligible=p[P_ELIG], split=split, count_after=glob.count)
+
+
+def _launch_split(scene, mask, plan, pinned, take_cap, gidx, n, alpha, log_alpha, log_gamma,
+                  beta):
+    """publish the plan, then the guarded split and the children's global indices."""
+    _publish(plan, pinned)
+    if take_cap > 0:
+        _split_guarded(scene, mask, plan, alpha, log_alpha, log_gamma, beta)
+        _lib.check(_lib.lib().igs_shard_child_index(gidx.data_ptr(), n, plan.data_ptr(),
+                                                    _lib.stream_handle()),
+                   "densify_step_sharded")
 
 
 def _split_guarded(scene, mask, guard, alpha, log_alpha, log_gamma, beta):

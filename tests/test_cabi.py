@@ -85,3 +85,25 @@ def test_product_path_fails_loudly_without_gpu():
     import paper_2603_08661_b200 as igs
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         igs.importance_pipeline(np.zeros((8, 8, 3)))
+
+
+@pytest.mark.parametrize("cname,pyname", [("IgsLasSplitArgs", "LasSplitArgs"),
+                                          ("IgsShardEventArgs", "ShardEventArgs")])
+def test_packed_argument_structs_match_header(tmp_path, cname, pyname):
+    """The ctypes mirrors of the packed-argument structs have the header's size and field
+    offsets (a plain-C program compiled against include/igs_b200.h prints them)."""
+    import subprocess
+    from paper_2603_08661_b200 import _lib
+    py = getattr(_lib, pyname)
+    src = tmp_path / "off.c"
+    lines = [f'printf("%zu\\n", sizeof({cname}));']
+    lines += [f'printf("%zu\\n", offsetof({cname}, {f[0]}));' for f in py._fields_]
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "igs_b200.h"\n'
+                   "int main(void) {\n" + "\n".join(lines) + "\nreturn 0;\n}\n")
+    exe = tmp_path / "off"
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [C.sizeof(py)] + [getattr(py, f[0]).offset for f in py._fields_]
+    assert got == want
