@@ -94,3 +94,26 @@ def test_edge_score_assignment_checks_and_converts():
     assert len(st) == 6 and st.edge_score.shape == (6,)
     st.set_edge_score(np.ones(6))
     assert float(st.edge_score.sum()) == 6.0
+
+
+def test_stats_reset_writes_nothing_and_reads_zeros():
+    """DensifyStats.reset gives fresh statistics without a fill: stale buffer contents never
+    leak (pending rows read as zeros), old tensors keep their values (new buffers, as the
+    reference's new arrays), and assignments / accumulations see zeros underneath."""
+    from paper_2603_08661_b200.densify_controller import accumulate_grads
+    st = DensifyStats(5, device="cpu")
+    accumulate_grads(st, np.arange(5.0))
+    old = st._grad_sum
+    st.reset(7)
+    st._buf.fill_(float("nan"))                  # whatever the allocator hands back
+    assert torch.equal(old, torch.arange(5.0, dtype=torch.float64))
+    assert len(st) == 7 and st._accum_count == 0
+    assert torch.equal(st.grad_norm, torch.zeros(7, dtype=torch.float64))
+    st.edge_score = np.full(7, 0.5)
+    assert torch.equal(st.edge_score, torch.full((7,), 0.5, dtype=torch.float64))
+    assert torch.equal(st._grad_sum, torch.zeros(7, dtype=torch.float64))
+    st.reset()
+    st._buf.fill_(float("nan"))
+    accumulate_grads(st, np.full(7, 2.0))
+    assert torch.equal(st.grad_norm, torch.full((7,), 2.0, dtype=torch.float64))
+    assert torch.equal(st.edge_score, torch.zeros(7, dtype=torch.float64))
