@@ -491,11 +491,13 @@ __device__ unsigned long long block_select64(const unsigned long long (&v)[E], c
     }
     unsigned tot;
     unsigned long long cum = block_exclusive_scan(sum, warp_sums, &tot);
+    __shared__ unsigned s_cnt;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       if (loc[k] && rank >= cum && rank < cum + loc[k]) {
         *s_bin = threadIdx.x * PER + k;
         *s_val = rank - cum;
+        s_cnt = loc[k];
       }
       cum += loc[k];
     }
@@ -503,7 +505,17 @@ __device__ unsigned long long block_select64(const unsigned long long (&v)[E], c
     prefix |= (unsigned long long)(*s_bin) << shift;
     pmask |= (unsigned long long)dmask << shift;
     rank = *s_val;
+    const unsigned cnt = s_cnt;
     __syncthreads();
+    if (cnt == 1 && top >= RBITS) {  // one value left with this prefix: it is the answer (the
+                                     // boundary keys of a bucket usually separate in 1-2 rounds)
+      __shared__ unsigned long long s_res;
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (ok[k] && (v[k] & pmask) == prefix) s_res = v[k];
+      __syncthreads();
+      return s_res;
+    }
   }
   return prefix;
 }
