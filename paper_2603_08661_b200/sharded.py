@@ -168,37 +168,50 @@ class CudaShardOps:
     def event(self, records, comm, cap: int, n_global: int, gidx, scene, consts, pinned,
               split: bool):
         """finalize -> publish the plan -> (split, child indices) in one library call
-        (igs_shard_event); the same launches, in the same order, as the separate calls."""
+        (igs_shard_event); the same launches, in the same order, as the separate calls.  The
+        packed arguments are kept per instance; the scene / stream fields are rewritten only
+        when a column buffer, the constants or the stream change."""
         a = self.__dict__.get("_ev")
         if a is None:
             a = self._ev = _lib.ShardEventArgs()
             self._ev_addr = ctypes.addressof(a)
-        records = records.contiguous()
+            self._ev_key = None
+            a.mask, a.plan, a.n = self.mask.data_ptr(), self.plan.data_ptr(), self.n
+            a.shard_workspace, a.shard_workspace_bytes = self.ws.data_ptr(), self.ws.numel()
+            a.plan_words = PLAN_WORDS
+        if split:
+            cols = ((scene._pos, scene._ls, scene._rot, scene._op, scene._sh)
+                    if hasattr(scene, "_rot") else
+                    tuple(scene._cols[k] for k in ("positions", "log_scales", "thetas",
+                                                   "opacity_logits", "colors")))
+        else:
+            cols = ()
+        stream = _lib.stream_handle()
+        key = (cols, tuple(consts), stream, pinned[0].data_ptr())
+        old = self._ev_key
+        if (old is None or old[1:] != key[1:] or len(old[0]) != len(cols)
+                or any(x is not y for x, y in zip(old[0], cols))):
+            a.host_plan, a.stream = pinned[0].data_ptr(), stream
+            if cols:
+                (a.positions, a.log_scales, a.rotations, a.opacity_logits,
+                 a.sh_or_colors) = (t.data_ptr() for t in cols)
+                a.sh_floats, a.dims = (cols[4].shape[1] * 3, 3) if len(cols[2].shape) == 2 else (3, 2)
+                a.alpha, a.log_alpha, a.log_gamma, a.beta = consts
+            self._ev_key = key
+        if not records.is_contiguous():
+            records = records.contiguous()
         self._ev_records = records          # alive until the next event on this stream
         a.records, a.world, a.rank = records.data_ptr(), comm.world, comm.rank
-        a.record_cap, a.n_global, a.gidx, a.n = int(cap), int(n_global), gidx.data_ptr(), self.n
-        a.mask, a.plan = self.mask.data_ptr(), self.plan.data_ptr()
-        a.shard_workspace, a.shard_workspace_bytes = self.ws.data_ptr(), self.ws.numel()
-        a.host_plan, a.plan_words = pinned[0].data_ptr(), PLAN_WORDS
+        a.record_cap, a.n_global, a.gidx = cap, n_global, gidx.data_ptr()
         a.split = 1 if split else 0
-        if split:
-            if hasattr(scene, "_rot"):
-                cols = (scene._pos, scene._ls, scene._rot, scene._op, scene._sh)
-                a.sh_floats, a.dims = scene._sh.shape[1] * 3, 3
-            else:
-                c2 = scene._cols
-                cols = (c2["positions"], c2["log_scales"], c2["thetas"], c2["opacity_logits"],
-                        c2["colors"])
-                a.sh_floats, a.dims = 3, 2
-            (a.positions, a.log_scales, a.rotations, a.opacity_logits,
-             a.sh_or_colors) = (t.data_ptr() for t in cols)
-            a.reserved_rows = scene.reserved_rows
-            a.alpha, a.log_alpha, a.log_gamma, a.beta = consts
+        if split:  # the shared LAS scratch can be regrown by other calls: looked up every time
             ws = _lib.workspace(_lib.query_size(self.L.igs_las_workspace_bytes, self.n),
                                 self.device, "las")
             a.las_workspace, a.las_workspace_bytes = ws.data_ptr(), ws.numel()
-        a.stream = _lib.stream_handle()
-        _lib.check(self.L.igs_shard_event(self._ev_addr), "densify_step_sharded")
+            a.reserved_rows = scene.reserved_rows
+        rc = self.L.igs_shard_event(self._ev_addr)
+        if rc:
+            _lib.check(rc, "densify_step_sharded")
         return self.mask, self.plan
 
 
