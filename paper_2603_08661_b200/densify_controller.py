@@ -60,6 +60,14 @@ class DensifyStats:
     def _grad_sum(self) -> torch.Tensor:
         return self._row(0)
 
+    def _ptr(self, k: int) -> int:
+        """Device address of row k (0: gradient sums, 1: edge scores) for the kernels, zeroed
+        first if pending (no tensor view built on the launch path)."""
+        if self._pending[k]:
+            self._buf[k].zero_()
+            self._pending[k] = False
+        return self._buf.data_ptr() + k * self._buf.stride(0) * 8
+
     def __len__(self):
         return self._buf.shape[1]
 
@@ -145,7 +153,7 @@ def _launch_select(stats: DensifyStats, cfg: DensifyConfig, step: int, take_cap:
     nbytes = _lib.query_size(L.igs_select_workspace_bytes, n)
     ws = _lib.workspace(nbytes, stats._device, "select")
     _lib.check(L.igs_select_candidates(
-        stats._grad_sum.data_ptr(), stats._accum_count, stats.edge_score.data_ptr(), n,
+        stats._ptr(0), stats._accum_count, stats._ptr(1), n,
         float(cfg.grad_threshold), int(is_warmup_step(cfg, step)), _lib.IGS_POLICY[cfg.policy],
         int(take_cap), mask.data_ptr(), counts.data_ptr(), ws.data_ptr(), ws.numel(),
         _lib.stream_handle()), "select_candidates")

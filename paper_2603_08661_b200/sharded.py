@@ -137,7 +137,7 @@ class CudaShardOps:
 
     def keys(self, stats: DensifyStats, cfg: DensifyConfig, step: int) -> torch.Tensor:
         _lib.check(self.L.igs_shard_keys(
-            stats._grad_sum.data_ptr(), stats._accum_count, stats.edge_score.data_ptr(), self.n,
+            stats._ptr(0), stats._accum_count, stats._ptr(1), self.n,
             float(cfg.grad_threshold), int(is_warmup_step(cfg, step)),
             _lib.IGS_POLICY[cfg.policy], self.hist.data_ptr(), self.ws.data_ptr(),
             self.ws.numel(), _lib.stream_handle()), "densify_step_sharded")
@@ -457,7 +457,9 @@ def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: i
     alpha, log_alpha, log_gamma, beta = c.device_constants()
     gidx = scene._gidx
     cap = default_record_cap(comm.world)
-    pinned = _las.pinned_summary(scene.device, PLAN_WORDS + 1)
+    pinned = ops.__dict__.get("_pinned")
+    if pinned is None:
+        pinned = ops._pinned = _las.pinned_summary(scene.device, PLAN_WORDS + 1)
     hist, records = _exchange(ops, stats, cfg, step, take_cap, comm, gidx, scene, beta, cap)
     if isinstance(ops, CudaShardOps):   # finalize, publish, split, child indices: one call
         mask, plan = ops.event(records, comm, cap, glob.count, gidx, scene,
