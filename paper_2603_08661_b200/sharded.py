@@ -187,27 +187,27 @@ class CudaShardOps:
         else:
             cols = ()
         stream = _lib.stream_handle()
-        key = (cols, tuple(consts), stream, pinned[0].data_ptr())
         old = self._ev_key
-        if (old is None or old[1:] != key[1:] or len(old[0]) != len(cols)
-                or any(x is not y for x, y in zip(old[0], cols))):
+        if (old is None or old[1] != consts or old[2] != stream or old[3] is not pinned
+                or len(old[0]) != len(cols) or any(x is not y for x, y in zip(old[0], cols))):
             a.host_plan, a.stream = pinned[0].data_ptr(), stream
             if cols:
                 (a.positions, a.log_scales, a.rotations, a.opacity_logits,
                  a.sh_or_colors) = (t.data_ptr() for t in cols)
                 a.sh_floats, a.dims = (cols[4].shape[1] * 3, 3) if len(cols[2].shape) == 2 else (3, 2)
                 a.alpha, a.log_alpha, a.log_gamma, a.beta = consts
-            self._ev_key = key
-        if not records.is_contiguous():
-            records = records.contiguous()
+                if self.__dict__.get("_las_ws") is None:  # this shard's own LAS scratch
+                    self._las_ws = torch.empty(
+                        max(_lib.query_size(self.L.igs_las_workspace_bytes, self.n), 256),
+                        dtype=torch.uint8, device=self.device)
+                a.las_workspace = self._las_ws.data_ptr()
+                a.las_workspace_bytes = self._las_ws.numel()
+            self._ev_key = (cols, consts, stream, pinned)
         self._ev_records = records          # alive until the next event on this stream
         a.records, a.world, a.rank = records.data_ptr(), comm.world, comm.rank
         a.record_cap, a.n_global, a.gidx = cap, n_global, gidx.data_ptr()
         a.split = 1 if split else 0
-        if split:  # the shared LAS scratch can be regrown by other calls: looked up every time
-            ws = _lib.workspace(_lib.query_size(self.L.igs_las_workspace_bytes, self.n),
-                                self.device, "las")
-            a.las_workspace, a.las_workspace_bytes = ws.data_ptr(), ws.numel()
+        if split:
             a.reserved_rows = scene.reserved_rows
         rc = self.L.igs_shard_event(self._ev_addr)
         if rc:
@@ -460,11 +460,15 @@ def densify_step_sharded(scene, stats: DensifyStats, cfg: DensifyConfig, step: i
     pinned = ops.__dict__.get("_pinned")
     if pinned is None:
         pinned = ops._pinned = _las.pinned_summary(scene.device, PLAN_WORDS + 1)
-    hist, records = _exchange(ops, stats, cfg, step, take_cap, comm, gidx, scene, beta, cap)
     if isinstance(ops, CudaShardOps):   # finalize, publish, split, child indices: one call
+        hist = comm.all_reduce_sum_(ops.keys(stats, cfg, step))             # round 1
+        rec = ops.boundary(hist, take_cap, gidx, scene, beta, cap)
+        records = comm.all_gather(rec).contiguous() if comm.world > 1 else rec  # round 2
         mask, plan = ops.event(records, comm, cap, glob.count, gidx, scene,
                                (alpha, log_alpha, log_gamma, beta), pinned, take_cap > 0)
     else:
+        hist, records = _exchange(ops, stats, cfg, step, take_cap, comm, gidx, scene, beta,
+                                  cap)
         mask, plan = ops.finalize(records, comm.rank, cap, glob.count, gidx)
         _launch_split(scene, mask, plan, pinned, take_cap, gidx, n, alpha, log_alpha, log_gamma,
                       beta)
